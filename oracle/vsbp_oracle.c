@@ -1,0 +1,510 @@
+/*
+ * vsbp_oracle.c -- the CPU ORACLE for the stereo hot path of arXiv 1902.09733.
+ *
+ * TEST INFRASTRUCTURE ONLY.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  The product path
+ * (paper_1902_09733_b200/) never links, imports or executes it, and shares no code,
+ * header, table or constant with it.
+ *
+ * Plain, slow, obviously-correct C: scalar loops, no blocking, no fusion, no SIMD,
+ * no threads.  Integer BP in int32 fixed point; JBU and reprojection in double.
+ *
+ * Citations: P:n = /root/reference/PAPER.md line n; S:n = SPEC.md line n;
+ * DESIGN.md "Readings" R-n = the reading adopted where the paper is silent.
+ *
+ * Layouts (all row-major, tightly packed, host memory owned by the caller):
+ *   images          u8  [H][W]            (grey)      u8 [H][W][3] (RGB)
+ *   cost volume D   i32 [H][W][L]
+ *   messages M      i32 [4][H][W][L]      M[k][y][x][d] = message pixel (x,y)
+ *                                          SENDS toward direction k
+ *                                          k: 0 up (y-1), 1 down (y+1),
+ *                                             2 left (x-1), 3 right (x+1)
+ *   disparity       i32 [H][W] labels;    upsampled: double [sH][sW] full-res px
+ *   xyz             double [H][W][3]
+ *
+ * Error codes: 0 ok, -1 invalid argument, -2 dimension mismatch, -3 overflow.
+ *
+ * Parity pins for every function: tests/test_oracle_pins.py.
+ */
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+#include <math.h>
+
+#define OR_OK 0
+#define OR_EINVAL (-1)
+#define OR_EDIM (-2)
+#define OR_EOVERFLOW (-3)
+
+/* Fixed-point scale S = 2^7 (R-6): one label of disparity difference
+ * costs S in the smoothness term.  Paper: silent on numerics. */
+#define ORACLE_FIXED_SHIFT 7
+
+/* ------------------------------------------------------------------------- */
+/* O1  parameter quantisation (R-5, R-6, R-7)                        */
+/* ------------------------------------------------------------------------- */
+
+/* round half away from zero, evaluated in double */
+static int64_t round_half_away(double v)
+{
+    if (v >= 0.0)
+        return (int64_t)floor(v + 0.5);
+    return -(int64_t)floor(-v + 0.5);
+}
+
+/* out[0] = lambda_q = round(lambda * S)   (weight of the data term, R-5)
+ * out[1] = tau_d    = round(data_trunc)   (intensity levels)
+ * out[2] = tau_q    = round(disc_trunc*S) (smoothness truncation, fixed point)
+ * out[3] = S        = 2^7                 (smoothness slope per label)       */
+int oracle_quantize(float lambda, float data_trunc, float disc_trunc, int32_t out[4])
+{
+    const double S = (double)(1 << ORACLE_FIXED_SHIFT);
+    if (!out) return OR_EINVAL;
+    if (!(lambda >= 0.0f) || !(data_trunc > 0.0f) || !(disc_trunc > 0.0f)) return OR_EINVAL;
+    int64_t lq = round_half_away((double)lambda * S);
+    int64_t td = round_half_away((double)data_trunc);
+    int64_t tq = round_half_away((double)disc_trunc * S);
+    if (td < 1 || tq < 1) return OR_EINVAL;
+    if (lq > 0x7fffffff || td > 0x7fffffff || tq > 0x7fffffff) return OR_EOVERFLOW;
+    out[0] = (int32_t)lq;
+    out[1] = (int32_t)td;
+    out[2] = (int32_t)tq;
+    out[3] = (int32_t)S;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O0  prep: RGB -> grey -> s x s box mean  ("downsample the stereo  */
+/*     image pairs"; R-22: BT.601 integer grey, area average)      */
+/* ------------------------------------------------------------------------- */
+int oracle_prep(const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray_lo)
+{
+    if (!rgb || !gray_lo || W_hi < 1 || H_hi < 1 || s < 1) return OR_EINVAL;
+    if (W_hi % s != 0 || H_hi % s != 0) return OR_EDIM;
+    int W = W_hi / s, H = H_hi / s;
+    for (int Y = 0; Y < H; ++Y) {
+        for (int X = 0; X < W; ++X) {
+            int64_t sum = 0;
+            for (int j = 0; j < s; ++j) {
+                for (int i = 0; i < s; ++i) {
+                    const uint8_t *px = rgb + 3 * ((size_t)(Y * s + j) * W_hi + (size_t)(X * s + i));
+                    int g = (77 * px[0] + 150 * px[1] + 29 * px[2] + 128) >> 8;
+                    sum += g;
+                }
+            }
+            int64_t n = (int64_t)s * s;
+            gray_lo[(size_t)Y * W + X] = (uint8_t)((sum + n / 2) / n);
+        }
+    }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O2  data cost E_{D,X}(d)  (Eq.1; R-2 truncated AD, R-8 border)     */
+/* D(x,y,d) = lambda_q * min(|L(x,y) - R(x-d,y)|, tau_d)  if x-d >= 0          */
+/*          = lambda_q * tau_d                             otherwise           */
+/* ------------------------------------------------------------------------- */
+int oracle_cost_volume(const uint8_t *left, const uint8_t *right, int W, int H, int L,
+                       int32_t lam_q, int32_t tau_d, int32_t *D)
+{
+    if (!left || !right || !D || W < 1 || H < 1 || L < 2 || lam_q < 0 || tau_d < 1) return OR_EINVAL;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x)
+            for (int d = 0; d < L; ++d) {
+                int32_t c;
+                if (x - d >= 0) {
+                    int diff = abs((int)left[(size_t)y * W + x] - (int)right[(size_t)y * W + (x - d)]);
+                    c = lam_q * (diff < tau_d ? diff : tau_d);
+                } else {
+                    c = lam_q * tau_d;
+                }
+                D[((size_t)y * W + x) * L + d] = c;
+            }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O3  cost pyramid  ("[4]" hierarchical BP; R-12)                        */
+/* W' = ceil(W/2), H' = ceil(H/2);  D'(X,Y,d) = sum of D over the existing     */
+/* children (2X+i, 2Y+j), i,j in {0,1}.                                        */
+/* ------------------------------------------------------------------------- */
+int oracle_pyramid_down(const int32_t *D, int W, int H, int L, int32_t *Dn)
+{
+    if (!D || !Dn || W < 1 || H < 1 || L < 1) return OR_EINVAL;
+    int Wn = (W + 1) / 2, Hn = (H + 1) / 2;
+    for (int Y = 0; Y < Hn; ++Y)
+        for (int X = 0; X < Wn; ++X)
+            for (int d = 0; d < L; ++d) {
+                int64_t sum = 0;
+                for (int j = 0; j < 2; ++j)
+                    for (int i = 0; i < 2; ++i) {
+                        int x = 2 * X + i, y = 2 * Y + j;
+                        if (x < W && y < H) sum += D[((size_t)y * W + x) * L + d];
+                    }
+                if (sum > 0x7fffffff) return OR_EOVERFLOW;
+                Dn[((size_t)Y * Wn + X) * L + d] = (int32_t)sum;
+            }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4  one message  (Eq.1 "M_{Y,X}(d) is the message vector passed     */
+/* from a pixel to its neighbor"; R-3 truncated linear smoothness, R-9 min-    */
+/* normalisation; S:137-145, S:168 two-pass O(L) distance transform)           */
+/*                                                                             */
+/*   m(d) = min( min_{d'} h(d') + S*|d-d'| ,  min_{d'} h(d') + tau_q ) - min h */
+/*                                                                             */
+/* The inner min over d' is the lower envelope of cones computed by the two-   */
+/* pass distance transform: f(d) = min(h(d), f(d-1)+S) forward, then           */
+/* g(d) = min(f(d), g(d+1)+S) backward.                                        */
+/* ------------------------------------------------------------------------- */
+int oracle_message(const int32_t *h, int L, int32_t S, int32_t tau_q, int32_t *m)
+{
+    if (!h || !m || L < 1 || S < 0 || tau_q < 0) return OR_EINVAL;
+    int32_t *g = (int32_t *)malloc(sizeof(int32_t) * (size_t)L);
+    if (!g) return OR_EINVAL;
+    /* forward pass */
+    g[0] = h[0];
+    for (int d = 1; d < L; ++d) {
+        int32_t a = h[d], b = g[d - 1] + S;
+        g[d] = a < b ? a : b;
+    }
+    /* backward pass */
+    for (int d = L - 2; d >= 0; --d) {
+        int32_t b = g[d + 1] + S;
+        if (b < g[d]) g[d] = b;
+    }
+    int32_t hmin = h[0];
+    for (int d = 1; d < L; ++d)
+        if (h[d] < hmin) hmin = h[d];
+    for (int d = 0; d < L; ++d) {
+        int32_t t = hmin + tau_q;
+        int32_t v = g[d] < t ? g[d] : t;
+        m[d] = v - hmin;
+    }
+    free(g);
+    return OR_OK;
+}
+
+/* neighbour of (x,y) in direction k; returns 0 if it does not exist */
+static int neighbour(int x, int y, int k, int W, int H, int *nx, int *ny)
+{
+    static const int dx[4] = {0, 0, -1, 1};
+    static const int dy[4] = {-1, 1, 0, 0};
+    int qx = x + dx[k], qy = y + dy[k];
+    if (qx < 0 || qy < 0 || qx >= W || qy >= H) return 0;
+    *nx = qx;
+    *ny = qy;
+    return 1;
+}
+
+/* the direction in which neighbour q (lying in direction k of p) sends back to p */
+static int opposite(int k)
+{
+    static const int opp[4] = {1, 0, 3, 2};
+    return opp[k];
+}
+
+#define MSG(M, k, x, y, W, H, L) ((M) + ((((size_t)(k) * (H) + (y)) * (W) + (x)) * (L)))
+
+/* incoming message to p=(x,y) from its neighbour in direction k (0 if none),
+ * copied into in[0..L) */
+static void incoming(const int32_t *M, int x, int y, int k, int W, int H, int L, int32_t *in)
+{
+    int qx, qy;
+    if (!neighbour(x, y, k, W, H, &qx, &qy)) {
+        for (int d = 0; d < L; ++d) in[d] = 0;
+        return;
+    }
+    const int32_t *src = MSG(M, opposite(k), qx, qy, W, H, L);
+    for (int d = 0; d < L; ++d) in[d] = src[d];
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4  checkerboard BP on one level  (Eq.1, "maximum iteration is */
+/* set to 5"; R-10 schedule, R-11 borders)                                     */
+/* Iteration t updates every pixel with (x+y+t) mod 2 == 0, in place.  For     */
+/* each existing neighbour q (direction k):                                    */
+/*   h(d) = D(p,d) + sum_{j != k} in_j(d);  M[k][p] = message(h)               */
+/* Messages toward non-existent neighbours are 0 and never computed.           */
+/* ------------------------------------------------------------------------- */
+int oracle_bp_level(const int32_t *D, int W, int H, int L, int32_t S, int32_t tau_q,
+                    int iters, int t0, int32_t *M)
+{
+    if (!D || !M || W < 1 || H < 1 || L < 1 || iters < 0) return OR_EINVAL;
+    int32_t *in = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)L);
+    int32_t *h = (int32_t *)malloc(sizeof(int32_t) * (size_t)L);
+    if (!in || !h) { free(in); free(h); return OR_EINVAL; }
+    for (int t = t0; t < t0 + iters; ++t) {
+        for (int y = 0; y < H; ++y) {
+            for (int x = 0; x < W; ++x) {
+                if ((x + y + t) % 2 != 0) continue;
+                for (int k = 0; k < 4; ++k) incoming(M, x, y, k, W, H, L, in + (size_t)k * L);
+                for (int k = 0; k < 4; ++k) {
+                    int qx, qy;
+                    int32_t *out = MSG(M, k, x, y, W, H, L);
+                    if (!neighbour(x, y, k, W, H, &qx, &qy)) {
+                        for (int d = 0; d < L; ++d) out[d] = 0;
+                        continue;
+                    }
+                    for (int d = 0; d < L; ++d) {
+                        int32_t v = D[((size_t)y * W + x) * L + d];
+                        for (int j = 0; j < 4; ++j)
+                            if (j != k) v += in[(size_t)j * L + d];
+                        h[d] = v;
+                    }
+                    oracle_message(h, L, S, tau_q, out);
+                }
+            }
+        }
+    }
+    free(in);
+    free(h);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O4  message initialisation of level l from level l+1 (R-12):                */
+/*   m^l_{p,k} = m^{l+1}_{P(p),k}  if p has a neighbour in direction k, else 0 */
+/*   P(x,y) = (floor(x/2), floor(y/2)).                                        */
+/* ------------------------------------------------------------------------- */
+int oracle_upcopy(const int32_t *Mp, int Wp, int Hp, int W, int H, int L, int32_t *M)
+{
+    if (!Mp || !M || W < 1 || H < 1 || L < 1) return OR_EINVAL;
+    if (Wp != (W + 1) / 2 || Hp != (H + 1) / 2) return OR_EDIM;
+    for (int k = 0; k < 4; ++k)
+        for (int y = 0; y < H; ++y)
+            for (int x = 0; x < W; ++x) {
+                int qx, qy;
+                int32_t *dst = MSG(M, k, x, y, W, H, L);
+                if (!neighbour(x, y, k, W, H, &qx, &qy)) {
+                    for (int d = 0; d < L; ++d) dst[d] = 0;
+                    continue;
+                }
+                const int32_t *src = MSG(Mp, k, x / 2, y / 2, Wp, Hp, L);
+                for (int d = 0; d < L; ++d) dst[d] = src[d];
+            }
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O6  WTA  ("the label d that minimizes E_X(d) is assigned to each pixel"; */
+/* Eq.1 E_X(d) = E_D,X(d) + sum_{Y in N(X)} M_{Y,X}(d); R-13 ties -> smallest d) */
+/* ------------------------------------------------------------------------- */
+int oracle_wta(const int32_t *D, const int32_t *M, int W, int H, int L, int32_t *disp)
+{
+    if (!D || !M || !disp || W < 1 || H < 1 || L < 1) return OR_EINVAL;
+    int32_t *in = (int32_t *)malloc(sizeof(int32_t) * 4 * (size_t)L);
+    if (!in) return OR_EINVAL;
+    for (int y = 0; y < H; ++y)
+        for (int x = 0; x < W; ++x) {
+            for (int k = 0; k < 4; ++k) incoming(M, x, y, k, W, H, L, in + (size_t)k * L);
+            int best = 0;
+            int64_t bestv = 0;
+            for (int d = 0; d < L; ++d) {
+                int64_t e = D[((size_t)y * W + x) * L + d];
+                for (int k = 0; k < 4; ++k) e += in[(size_t)k * L + d];
+                if (d == 0 || e < bestv) { bestv = e; best = d; }
+            }
+            disp[(size_t)y * W + x] = best;
+        }
+    free(in);
+    return OR_OK;
+}
+
+/* number of int32 entries of the per-level message fields, all levels */
+static size_t level_dims(int W, int H, int levels, int *Ws, int *Hs)
+{
+    size_t total = 0;
+    int w = W, h = H;
+    for (int l = 0; l < levels; ++l) {
+        Ws[l] = w;
+        Hs[l] = h;
+        total += (size_t)w * h;
+        w = (w + 1) / 2;
+        h = (h + 1) / 2;
+    }
+    return total;
+}
+
+/* ------------------------------------------------------------------------- */
+/* Full hierarchical BP disparity  ("perform stereo matching on low   */
+/* resolution image pairs", "GPU based Belief Propagation [4]", Eq.1, WTA)     */
+/*   D_0 = cost volume; D_{l+1} = pyramid(D_l);                                */
+/*   top level: M = 0; level l < top: M = upcopy(M_{l+1});                      */
+/*   each level: iters checkerboard iterations, t = 0..iters-1;                */
+/*   disp = WTA(D_0, M_0).                                                     */
+/* msgs_out (optional): all levels' final message fields, level 0 first, each   */
+/* [4][H_l][W_l][L] int32.                                                     */
+/* ------------------------------------------------------------------------- */
+int oracle_bp_disparity(const uint8_t *left, const uint8_t *right, int W, int H, int L,
+                        int levels, int iters, float lambda, float data_trunc, float disc_trunc,
+                        int32_t *disp, int32_t *msgs_out)
+{
+    if (!left || !right || !disp || W < 1 || H < 1 || L < 2 || levels < 1 || levels > 16 || iters < 1)
+        return OR_EINVAL;
+    int32_t q[4];
+    int rc = oracle_quantize(lambda, data_trunc, disc_trunc, q);
+    if (rc) return rc;
+    int32_t lam_q = q[0], tau_d = q[1], tau_q = q[2], S = q[3];
+    /* int32 bound (R-12 / O5): the largest belief at the top level must fit */
+    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q;
+    if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
+
+    int Ws[16], Hs[16];
+    level_dims(W, H, levels, Ws, Hs);
+    int32_t *Dl[16] = {0}, *Ml[16] = {0};
+    rc = OR_OK;
+    for (int l = 0; l < levels; ++l) {
+        size_t n = (size_t)Ws[l] * Hs[l] * L;
+        Dl[l] = (int32_t *)malloc(sizeof(int32_t) * n);
+        Ml[l] = (int32_t *)calloc(4 * n, sizeof(int32_t));
+        if (!Dl[l] || !Ml[l]) { rc = OR_EINVAL; goto done; }
+    }
+    rc = oracle_cost_volume(left, right, W, H, L, lam_q, tau_d, Dl[0]);
+    if (rc) goto done;
+    for (int l = 0; l + 1 < levels; ++l) {
+        rc = oracle_pyramid_down(Dl[l], Ws[l], Hs[l], L, Dl[l + 1]);
+        if (rc) goto done;
+    }
+    for (int l = levels - 1; l >= 0; --l) {
+        if (l < levels - 1) {
+            rc = oracle_upcopy(Ml[l + 1], Ws[l + 1], Hs[l + 1], Ws[l], Hs[l], L, Ml[l]);
+            if (rc) goto done;
+        }
+        rc = oracle_bp_level(Dl[l], Ws[l], Hs[l], L, S, tau_q, iters, 0, Ml[l]);
+        if (rc) goto done;
+    }
+    rc = oracle_wta(Dl[0], Ml[0], W, H, L, disp);
+    if (rc) goto done;
+    if (msgs_out) {
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            size_t n = 4 * (size_t)Ws[l] * Hs[l] * L;
+            memcpy(msgs_out + off, Ml[l], sizeof(int32_t) * n);
+            off += n;
+        }
+    }
+done:
+    for (int l = 0; l < levels; ++l) { free(Dl[l]); free(Ml[l]); }
+    return rc;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O7  joint bilateral upsampling  (Eq.2; P:84 JBF parameters;          */
+/* R-15..R-19)                                                                 */
+/*   p = (x,y) full-res; p_down = ((x+0.5)/s - 0.5, (y+0.5)/s - 0.5);           */
+/*   window centre c = (floor(x/s), floor(y/s)); taps q in [c-r, c+r]^2 inside  */
+/*   the low-res image; I_q = guide at (s*qx + floor(s/2), s*qy + floor(s/2));  */
+/*   logit(q) = -|p_down - q|^2/(2 sigma_s^2) - |I_p - I_q|^2/(2 sigma_r^2)     */
+/*   (Euclidean RGB distance, 0..255 scale);                                    */
+/*   D_p = s * sum_q w_q D'_q / sum_q w_q,  w_q = exp(logit(q) - max_q logit)  */
+/* (the max-subtraction cancels in the ratio: it is Eq.2 with K_p = sum w).     */
+/* ------------------------------------------------------------------------- */
+int oracle_jbu(const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s,
+               double sigma_s, double sigma_r, int radius, double *disp_hi)
+{
+    if (!disp_lo || !guide || !disp_hi || W < 1 || H < 1 || s < 1 || radius < 1) return OR_EINVAL;
+    if (!(sigma_s > 0.0) || !(sigma_r > 0.0)) return OR_EINVAL;
+    int Wh = W * s, Hh = H * s;
+    int ntap = (2 * radius + 1) * (2 * radius + 1);
+    double *logit = (double *)malloc(sizeof(double) * (size_t)ntap);
+    double *val = (double *)malloc(sizeof(double) * (size_t)ntap);
+    if (!logit || !val) { free(logit); free(val); return OR_EINVAL; }
+    for (int y = 0; y < Hh; ++y) {
+        for (int x = 0; x < Wh; ++x) {
+            double px = ((double)x + 0.5) / (double)s - 0.5;
+            double py = ((double)y + 0.5) / (double)s - 0.5;
+            int cx = x / s, cy = y / s;
+            const uint8_t *Ip = guide + 3 * ((size_t)y * Wh + x);
+            int n = 0;
+            double lmax = -INFINITY;
+            for (int qy = cy - radius; qy <= cy + radius; ++qy) {
+                for (int qx = cx - radius; qx <= cx + radius; ++qx) {
+                    if (qx < 0 || qy < 0 || qx >= W || qy >= H) continue;
+                    int gx = s * qx + s / 2, gy = s * qy + s / 2;
+                    const uint8_t *Iq = guide + 3 * ((size_t)gy * Wh + gx);
+                    double dr = (double)Ip[0] - Iq[0], dg = (double)Ip[1] - Iq[1], db = (double)Ip[2] - Iq[2];
+                    double range2 = dr * dr + dg * dg + db * db;
+                    double sx = px - qx, sy = py - qy;
+                    double spat2 = sx * sx + sy * sy;
+                    double l = -spat2 / (2.0 * sigma_s * sigma_s) - range2 / (2.0 * sigma_r * sigma_r);
+                    logit[n] = l;
+                    val[n] = (double)disp_lo[(size_t)qy * W + qx];
+                    if (l > lmax) lmax = l;
+                    ++n;
+                }
+            }
+            double num = 0.0, den = 0.0;
+            for (int i = 0; i < n; ++i) {
+                double w = exp(logit[i] - lmax);
+                num += w * val[i];
+                den += w;
+            }
+            disp_hi[(size_t)y * Wh + x] = (double)s * num / den;
+        }
+    }
+    free(logit);
+    free(val);
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* O8  reprojection  (Eq.3; R-20 z = f*B/(d*du); R-21 min_disp)         */
+/*   [X Y Z Wh]^T = Q [u v d 1]^T;  xyz = (X,Y,Z)/Wh if d >= min_disp else NaN  */
+/* Q is row-major 4x4.                                                         */
+/* ------------------------------------------------------------------------- */
+int oracle_reproject(const double *disp, int W, int H, const double *Q, double min_disp,
+                     double *xyz, int64_t *n_valid)
+{
+    if (!disp || !Q || !xyz || !n_valid || W < 1 || H < 1) return OR_EINVAL;
+    if (!(min_disp > 0.0)) return OR_EINVAL;
+    int64_t count = 0;
+    for (int v = 0; v < H; ++v)
+        for (int u = 0; u < W; ++u) {
+            double d = disp[(size_t)v * W + u];
+            double *o = xyz + 3 * ((size_t)v * W + u);
+            if (!(d >= min_disp)) {
+                o[0] = o[1] = o[2] = NAN;
+                continue;
+            }
+            double in[4] = {(double)u, (double)v, d, 1.0}, out[4];
+            for (int r = 0; r < 4; ++r) {
+                out[r] = 0.0;
+                for (int c = 0; c < 4; ++c) out[r] += Q[4 * r + c] * in[c];
+            }
+            o[0] = out[0] / out[3];
+            o[1] = out[1] / out[3];
+            o[2] = out[2] / out[3];
+            ++count;
+        }
+    *n_valid = count;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
+/* a8  per-pair summary: label sum and an order-independent    */
+/* 64-bit hash of the low-res disparity, hash = sum_i mix(i << 32 | label_i)    */
+/* mod 2^64, mix = SplitMix64 finaliser.                                       */
+/* ------------------------------------------------------------------------- */
+static uint64_t oracle_mix64(uint64_t z)
+{
+    z += 0x9E3779B97F4A7C15ULL;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ULL;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBULL;
+    return z ^ (z >> 31);
+}
+
+int oracle_disp_summary(const int32_t *disp, int W, int H, int64_t *label_sum, uint64_t *label_hash)
+{
+    if (!disp || !label_sum || !label_hash || W < 1 || H < 1) return OR_EINVAL;
+    int64_t sum = 0;
+    uint64_t hash = 0;
+    for (size_t i = 0; i < (size_t)W * H; ++i) {
+        sum += disp[i];
+        hash += oracle_mix64(((uint64_t)i << 32) | (uint32_t)disp[i]);
+    }
+    *label_sum = sum;
+    *label_hash = hash;
+    return OR_OK;
+}

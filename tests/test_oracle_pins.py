@@ -1,0 +1,372 @@
+"""Pins for the CPU oracle (-m "not gpu").  Each test checks the oracle against
+something other than itself: hand-worked or SPEC-printed values (tests/golden/),
+closed forms, invariants, textbook equivalences (Viterbi, Jacobi BP), exhaustive
+minimisation, or a literal evaluation of the paper's equation.
+lists which pin covers which oracle function."""
+import math
+
+import numpy as np
+import pytest
+
+import oracle
+import synthgen
+from brute import (beliefs, brute_message, chain_min_marginals, energy, exhaustive_map,
+                   jacobi_bp, jbu_literal, project)
+
+Q0 = oracle.quantize(0.07, 15.0, 1.7)
+
+
+# ----------------------------------------------------------------------------- O1
+def test_quantize_golden(golden):
+    for c in golden("quantize.json")["cases"]:
+        q = oracle.quantize(c["lambda"], c["data_trunc"], c["disc_trunc"])
+        assert [q.lam_q, q.tau_d, q.tau_q, q.S] == c["expect"]
+
+
+@pytest.mark.parametrize("args", [(-0.1, 15, 1.7), (0.07, 0.0, 1.7), (0.07, 15, 0.0), (0.07, 0.4, 1.7),
+                                  (0.07, 15, 0.003)])
+def test_quantize_rejects(args):
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.quantize(*args)
+    assert e.value.code == -1
+
+
+# ----------------------------------------------------------------------------- O0
+def test_prep_golden(golden):
+    g = golden("prep.json")
+    for c in g["grey"]:
+        rgb = np.array(c["rgb"], np.uint8).reshape(1, 1, 3)
+        assert int(oracle.prep(rgb, 1)[0, 0]) == c["g"]
+    blk = np.array(g["box2"]["grey_block"], np.uint8)
+    rgb = np.repeat(blk[:, :, None], 3, axis=2)  # grey (v,v,v) -> (256v+128)>>8 = v
+    assert int(oracle.prep(rgb, 2)[0, 0]) == g["box2"]["mean"]
+
+
+def test_prep_mean_and_constant():
+    rgb = np.full((12, 20, 3), 200, np.uint8)
+    assert np.all(oracle.prep(rgb, 4) == 200)
+    rgb = synthgen.value_noise_rgb(3, 64, 48)
+    grey = oracle.prep(rgb, 1).astype(np.float64)
+    lo = oracle.prep(rgb, 4).astype(np.float64)
+    # each block mean is within 0.5 of the exact mean of the grey block (rounding)
+    blocks = grey.reshape(12, 4, 16, 4).mean(axis=(1, 3))
+    assert np.max(np.abs(lo - blocks)) <= 0.5 + 1e-12
+    with pytest.raises(oracle.OracleError):
+        oracle.prep(np.zeros((10, 10, 3), np.uint8), 3)
+
+
+# ----------------------------------------------------------------------------- O2
+def test_cost_volume_special_cases():
+    q = oracle.QParams(lam_q=2, tau_d=15, tau_q=10, S=4)
+    left = np.array([[10, 20, 200]], np.uint8)
+    right = np.array([[15, 0, 190]], np.uint8)
+    D = oracle.cost_volume(left, right, 3, q)
+    # hand-worked: D(x,d) = 2*min(|L(x)-R(x-d)|, 15), border x-d<0 -> 2*15
+    expect = np.array([[[10, 30, 30], [30, 10, 30], [20, 30, 30]]])
+    assert np.array_equal(D, expect)
+
+    img = synthgen.iid_gray(5, 40, 30)
+    D = oracle.cost_volume(img, img, 16, Q0)
+    assert np.all(D[:, :, 0] == 0)  # S:134 identical images
+    l, r = synthgen.shifted_pair(6, 40, 30, 3)
+    D = oracle.cost_volume(l, r, 16, Q0)
+    assert np.all(D[:, 3:, 3] == 0)  # S:135 shifted texture
+    c = np.full((8, 20), 77, np.uint8)
+    D = oracle.cost_volume(c, c, 8, Q0)
+    x = np.arange(20)[None, :, None]
+    d = np.arange(8)[None, None, :]
+    assert np.array_equal(D[0:1], np.where(x >= d, 0, Q0.lam_q * Q0.tau_d).astype(np.int32))
+
+
+# ----------------------------------------------------------------------------- O3
+def test_pyramid_golden(golden):
+    g = golden("pyramid_3x3.json")
+    Dn = oracle.pyramid_down(np.array(g["D"], np.int32))
+    assert np.array_equal(Dn, np.array(g["Dn"], np.int32))
+
+
+@pytest.mark.parametrize("W,H", [(1, 1), (1, 7), (7, 1), (5, 3), (8, 6), (13, 9)])
+def test_pyramid_invariants(W, H):
+    rng = np.random.default_rng(W * 100 + H)
+    D = rng.integers(0, 1000, size=(H, W, 5)).astype(np.int32)
+    Dn = oracle.pyramid_down(D)
+    assert Dn.shape == ((H + 1) // 2, (W + 1) // 2, 5)
+    assert np.array_equal(Dn.sum(axis=(0, 1)), D.sum(axis=(0, 1)))  # mass per label
+    c = np.full((H, W, 2), 3, np.int32)
+    Cn = oracle.pyramid_down(c)
+    nx = np.array([min(2, W - 2 * X) for X in range((W + 1) // 2)])
+    ny = np.array([min(2, H - 2 * Y) for Y in range((H + 1) // 2)])
+    assert np.array_equal(Cn[:, :, 0], 3 * np.outer(ny, nx))  # children counted
+
+
+# ----------------------------------------------------------------------------- O4
+def test_message_golden(golden):
+    for c in golden("message_hand.json")["cases"]:
+        m = oracle.message(np.array(c["h"], np.int32), c["S"], c["tau_q"])
+        assert m.tolist() == c["m"], c
+
+
+def test_message_dt_equals_brute():
+    """the O(L) two-pass DT equals the O(L^2) minimisation exactly."""
+    rng = np.random.default_rng(0)
+    for it in range(3000):
+        L = int(rng.integers(1, 40))
+        S = int(rng.choice([1, 7, 128, 256]))
+        tau = int(rng.choice([1, 50, 218, 435, 5000, 1 << 20]))
+        h = rng.integers(0, int(rng.choice([10, 300, 3000, 100000])), size=L).astype(np.int32)
+        m = oracle.message(h, S, tau)
+        assert np.array_equal(m, brute_message(h, S, tau)), (h, S, tau)
+        assert m.min() == 0 and m.max() <= tau  # O5 invariants
+
+
+def test_zero_cost_fixed_point():
+    """all-zero costs keep all-zero messages for any number of iterations."""
+    D = np.zeros((5, 7, 6), np.int32)
+    M = oracle.bp_level(D, np.zeros((4, 5, 7, 6), np.int32), Q0.S, Q0.tau_q, 7)
+    assert not M.any()
+    img = np.full((9, 11), 50, np.uint8)
+    disp, msgs = oracle.bp_disparity(img, img, 4, 3, 4, lam=0.0, return_messages=True)
+    assert all(not m.any() for m in msgs)
+    assert not disp.any()  # ties -> smallest d (R-13)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_checkerboard_equals_jacobi(seed):
+    """Bipartite grid: checkerboard BP from zero messages equals synchronous BP
+    at step T on the colour updated last, and at step T-1 on the other colour."""
+    rng = np.random.default_rng(seed)
+    W, H, L = int(rng.integers(1, 6)), int(rng.integers(1, 5)), int(rng.integers(2, 6))
+    T = int(rng.integers(1, 7))
+    S, tau = int(rng.choice([1, 16, 128])), int(rng.integers(1, 400))
+    D = rng.integers(0, 600, size=(H, W, L)).astype(np.int32)
+    M = oracle.bp_level(D, np.zeros((4, H, W, L), np.int32), S, tau, T)
+    JT = jacobi_bp(D, S, tau, T)
+    JT1 = jacobi_bp(D, S, tau, T - 1)
+    last = (T - 1) % 2
+    for y in range(H):
+        for x in range(W):
+            ref = JT if (x + y) % 2 == last else JT1
+            assert np.array_equal(M[:, y, x], ref[:, y, x]), (seed, x, y)
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_chain_beliefs_are_viterbi_min_marginals(seed):
+    """H=1: tree BP is exact.  After >= 2W+2 checkerboard iterations the normalised
+    Eq.1 beliefs equal the exact min-marginals, and WTA is their argmin."""
+    rng = np.random.default_rng(100 + seed)
+    W, L = int(rng.integers(2, 13)), int(rng.integers(2, 7))
+    S, tau = int(rng.choice([16, 128])), int(rng.choice([100, 218, 400]))
+    D = rng.integers(0, 700, size=(1, W, L)).astype(np.int32)
+    M = oracle.bp_level(D, np.zeros((4, 1, W, L), np.int32), S, tau, 2 * W + 2)
+    b = beliefs(D, M)[0]
+    mu = chain_min_marginals(D[0], S, tau)
+    assert np.array_equal(b - b.min(axis=1, keepdims=True), mu - mu.min(axis=1, keepdims=True))
+    disp = oracle.wta(D, M)[0]
+    assert np.array_equal(disp, np.argmin(mu, axis=1))
+    # the WTA labelling is a global MAP of the chain (exhaustive check when tiny)
+    if L ** W <= 20000:
+        best, _ = exhaustive_map(D, S, tau)
+        assert energy(D, disp[None, :], S, tau) == best
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_hierarchical_chain_forgets_init(seed):
+    """levels > 1 on a 1-row image: the coarse-to-fine initialisation (pyramid +
+    up-copy) is forgotten by tree BP, so enough level-0 iterations still give the
+    exact min-marginals of the level-0 chain."""
+    rng = np.random.default_rng(200 + seed)
+    W, L = int(rng.integers(3, 14)), int(rng.integers(2, 7))
+    left = rng.integers(0, 256, size=(1, W), dtype=np.uint8)
+    right = rng.integers(0, 256, size=(1, W), dtype=np.uint8)
+    levels = int(rng.integers(2, 4))
+    disp, msgs = oracle.bp_disparity(left, right, L, levels, 2 * W + 2, return_messages=True)
+    D = oracle.cost_volume(left, right, L, Q0)
+    b = beliefs(D, msgs[0])[0]
+    mu = chain_min_marginals(D[0], Q0.S, Q0.tau_q)
+    assert np.array_equal(b - b.min(axis=1, keepdims=True), mu - mu.min(axis=1, keepdims=True))
+    assert np.array_equal(disp[0], np.argmin(mu, axis=1))
+
+
+def test_upcopy_hand_and_constant():
+    # hand-worked: parent 2x1 (L=1) right-messages [5, 0], left-messages [0, 7];
+    # child 3x1: x=0,1 -> parent 0, x=2 -> parent 1; slots toward missing neighbours are 0.
+    Mp = np.zeros((4, 1, 2, 1), np.int32)
+    Mp[3, 0, 0, 0] = 5
+    Mp[2, 0, 1, 0] = 7
+    M = oracle.upcopy(Mp, 3, 1)
+    assert M[3, 0, :, 0].tolist() == [5, 5, 0]
+    assert M[2, 0, :, 0].tolist() == [0, 0, 7]
+    assert not M[0].any() and not M[1].any()
+    Mp = np.full((4, 3, 4, 2), 9, np.int32)
+    M = oracle.upcopy(Mp, 7, 5)
+    ok = np.ones((4, 5, 7), bool)
+    ok[0, 0, :] = ok[1, 4, :] = ok[2, :, 0] = ok[3, :, 6] = False
+    assert np.array_equal(M[..., 0] == 9, ok) and np.array_equal(M[..., 0] == 0, ~ok)
+
+
+@pytest.mark.parametrize("seed", range(20))
+def test_strong_data_is_global_map(seed):
+    """If each pixel's data argmin beats every other label by > 4 tau_q, WTA equals
+    the data argmin, which is then the unique global MAP (exhaustive)."""
+    rng = np.random.default_rng(300 + seed)
+    H, W, L = 2, 3, 3
+    S, tau = 128, 218
+    D = rng.integers(4 * tau + 1, 4 * tau + 400, size=(H, W, L)).astype(np.int32)
+    best = rng.integers(0, L, size=(H, W))
+    np.put_along_axis(D, best[..., None], 0, axis=2)
+    M = oracle.bp_level(D, np.zeros((4, H, W, L), np.int32), S, tau, 5)
+    disp = oracle.wta(D, M)
+    assert np.array_equal(disp, best)
+    e, arg = exhaustive_map(D, S, tau)
+    assert len(arg) == 1 and np.array_equal(arg[0], best)
+
+
+def test_loopy_energy_never_below_global_min():
+    rng = np.random.default_rng(7)
+    for _ in range(30):
+        D = rng.integers(0, 600, size=(2, 3, 3)).astype(np.int32)
+        M = oracle.bp_level(D, np.zeros((4, 2, 3, 3), np.int32), 128, 218, 5)
+        disp = oracle.wta(D, M)
+        best, _ = exhaustive_map(D, 128, 218)
+        assert energy(D, disp, 128, 218) >= best
+
+
+def test_wta_zero_messages_is_data_argmin():
+    rng = np.random.default_rng(8)
+    D = rng.integers(0, 1000, size=(6, 7, 9)).astype(np.int32)
+    disp = oracle.wta(D, np.zeros((4, 6, 7, 9), np.int32))
+    assert np.array_equal(disp, np.argmin(D, axis=2))  # argmin returns the first: ties -> smallest
+
+
+def test_recovery_constant_shift_c1():
+    """BASELINE config 1 (64x48, L=16, 1 level, 5 iters), shift d0=5:
+    the known disparity is recovered on >= 99.9 % of pixels with x >= d0."""
+    l, r = synthgen.shifted_pair(1, 64, 48, 5)
+    disp = oracle.bp_disparity(l, r, 16, 1, 5)
+    frac = np.mean(disp[:, 5:] == 5)
+    assert frac >= 0.999, frac
+
+
+def test_recovery_row_plane_hierarchical():
+    """Row-wise integer plane on a 4-level pyramid: recovered away from row steps."""
+    l, r, drow = synthgen.row_plane_pair(2, 160, 120, 4, 27)
+    disp = oracle.bp_disparity(l, r, 32, 4, 5)
+    truth = np.broadcast_to(drow[:, None], disp.shape)
+    step = np.zeros(120, bool)
+    step[1:] |= drow[1:] != drow[:-1]
+    step[:-1] |= drow[1:] != drow[:-1]
+    valid = (np.arange(160)[None, :] >= 40) & ~step[:, None]
+    frac = np.mean(disp[valid] == truth[valid])
+    assert frac >= 0.999, frac
+
+
+def test_bp_overflow_and_args():
+    img = np.zeros((4, 4), np.uint8)
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.bp_disparity(img, img, 4, 12, 1, lam=1000.0, data_trunc=255.0)
+    assert e.value.code == -3
+    with pytest.raises(oracle.OracleError):
+        oracle.bp_disparity(img, img, 1, 1, 1)
+
+
+# ----------------------------------------------------------------------------- O7
+def test_jbu_matches_literal_eq2():
+    """random 4x4 low-res, random guide, vs Eq.2 evaluated literally (no
+    max-subtraction), s in {2,3}."""
+    rng = np.random.default_rng(9)
+    for s, r in [(2, 1), (3, 2), (2, 3)]:
+        lo = rng.integers(0, 30, size=(4, 4)).astype(np.int32)
+        guide = rng.integers(0, 256, size=(4 * s, 4 * s, 3), dtype=np.uint8)
+        got = oracle.jbu(lo, guide, s, 1.3, 40.0, r)
+        ref = jbu_literal(lo, guide, s, 1.3, 40.0, r)
+        assert np.max(np.abs(got - ref)) < 1e-12
+
+
+def test_jbu_properties():
+    rng = np.random.default_rng(10)
+    s = 4
+    guide = rng.integers(0, 256, size=(24, 32, 3), dtype=np.uint8)
+    const = np.full((6, 8), 11, np.int32)
+    assert np.allclose(oracle.jbu(const, guide, s, 3.75, 15.0, 2), s * 11, atol=1e-12, rtol=0)
+    lo = rng.integers(0, 60, size=(6, 8)).astype(np.int32)
+    out = oracle.jbu(lo, guide, s, 3.75, 15.0, 2)
+    assert out.min() >= s * lo.min() - 1e-9 and out.max() <= s * lo.max() + 1e-9  # convex hull
+    # constant guide -> spatial-only Gaussian (literal Eq.2 with g == 1)
+    flat = np.full_like(guide, 90)
+    assert np.max(np.abs(oracle.jbu(lo, flat, s, 3.75, 15.0, 2)
+                         - jbu_literal(lo, flat, s, 3.75, 1e9, 2))) < 1e-9
+    # mirror symmetry (odd s, where I_q sampling is mirror-symmetric)
+    s = 3
+    lo = rng.integers(0, 60, size=(5, 7)).astype(np.int32)
+    guide = rng.integers(0, 256, size=(15, 21, 3), dtype=np.uint8)
+    a = oracle.jbu(lo, guide, s, 2.0, 20.0, 2)
+    b = oracle.jbu(lo[:, ::-1].copy(), guide[:, ::-1].copy(), s, 2.0, 20.0, 2)
+    assert np.max(np.abs(a[:, ::-1] - b)) < 1e-9
+
+
+def test_jbu_edge_preservation():
+    """a disparity step co-located with a strong guide step (>= 5 sigma_r)
+    is preserved within 5 % of the step height next to the edge."""
+    s, W, H = 4, 16, 8
+    lo = np.where(np.arange(W)[None, :] < 8, 10, 30).astype(np.int32).repeat(H, axis=0)
+    guide = np.zeros((H * s, W * s, 3), np.uint8)
+    guide[:, : 8 * s] = 40
+    guide[:, 8 * s:] = 40 + 5 * 15
+    out = oracle.jbu(lo, guide, s, 3.75, 15.0, 2)
+    left, right = out[:, 8 * s - 1], out[:, 8 * s]
+    assert np.all(np.abs(left - s * 10) <= 0.05 * s * 20)
+    assert np.all(np.abs(right - s * 30) <= 0.05 * s * 20)
+
+
+# ----------------------------------------------------------------------------- O8
+def test_reproject_golden(golden):
+    g = golden("reproject_examples.json")
+    for c in g["reproject"]:
+        Q = oracle.q_matrix(c["f_du"], c["f_dv"], c["u0"], c["v0"], c["B"])
+        disp = np.zeros((c["v"] + 1, c["u"] + 1))
+        disp[c["v"], c["u"]] = c["d"]
+        xyz, n = oracle.reproject(disp, Q, 1.0)
+        assert n == 1
+        assert np.allclose(xyz[c["v"], c["u"]], c["xyz"], atol=1e-12)
+        disp[c["v"], c["u"]] = 2 * c["d"]  # S:257 doubling d halves xyz
+        xyz2, _ = oracle.reproject(disp, Q, 1.0)
+        assert np.allclose(xyz2[c["v"], c["u"]], np.array(c["xyz"]) / 2, atol=1e-12)
+    for c in g["project"]:
+        u, v, _ = project(c["xyz"], c["f_du"], c["f_dv"], c["u0"], c["v0"], c["B"])
+        assert (u, v) == tuple(c["uv"])
+
+
+def test_reproject_round_trip():
+    """project(first line of Eq.3) then reproject = identity to 1e-9."""
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"], 1390.0, I["u0"], I["v0"], I["B"])
+    rng = np.random.default_rng(11)
+    disp = np.zeros((40, 50))
+    pts = {}
+    for _ in range(200):
+        u, v = int(rng.integers(0, 50)), int(rng.integers(0, 40))
+        z = float(rng.uniform(5, 200))
+        x = (u - I["u0"]) * z / I["f_du"]
+        y = (v - I["v0"]) * z / 1390.0
+        uu, vv, d = project((x, y, z), I["f_du"], 1390.0, I["u0"], I["v0"], I["B"])
+        assert abs(uu - u) < 1e-9 and abs(vv - v) < 1e-9
+        disp[v, u] = d
+        pts[(u, v)] = (x, y, z)
+    xyz, n = oracle.reproject(disp, Q, 1.0)
+    for (u, v), p in pts.items():
+        assert np.allclose(xyz[v, u], p, rtol=1e-9, atol=1e-9)
+    assert n == int(np.sum(disp >= 1.0))
+    assert np.all(np.isnan(xyz[disp < 1.0]))
+    with pytest.raises(oracle.OracleError):
+        oracle.reproject(disp, Q, 0.0)
+
+
+# ----------------------------------------------------------------------------- a8
+def test_disp_summary_hash_known_value():
+    # SplitMix64 seeded with 0 yields 0xE220A8397B1DCDAF as its first output,
+    # which is mix(0) here: one pixel at index 0 with label 0.
+    s, h = oracle.disp_summary(np.zeros((1, 1), np.int32))
+    assert s == 0 and h == 0xE220A8397B1DCDAF
+    d = np.array([[3, 4]], np.int32)
+    s, _ = oracle.disp_summary(d)
+    assert s == 7
