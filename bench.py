@@ -1,0 +1,353 @@
+#!/usr/bin/env python
+"""bench.py -- 2.7K frame pairs/s of the stereo hot path (a0-a8) on 1..N B200s.
+
+Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl reference]`,
+torchrun for N > 1 (one rank per GPU, NCCL).  Rank 0 prints ONE JSON line.
+
+Workload (BASELINE.json configs[4], the metric's configuration, per GPU): a stream
+of synthetic 2.7K RGB virtual-stereo pairs; one step = one batch of B pairs per
+GPU through the whole path: prep (s=4) -> hierarchical BP 676x380, L=64, 5 levels
+x 5 iterations -> JBU r=2 to 2704x1520 -> reprojection -> per-pair summary, then
+an NCCL all_gather of the summaries (the only exchange).  Pairs are
+sharded round-robin (pair i -> rank i mod N): weak scaling.
+
+`value`  : pairs/s over all ranks, inputs resident in HBM, device-timed (CUDA
+           events on the launching stream, max over ranks).
+`e2e`    : the same through the public API with pinned HOST frames, H2D of the
+           step's RGB pairs and D2H of its summaries inside the timed region.
+`roofline`: the dominant kernel (level-0 message updates, a4): algorithmic bytes
+           / device time from live CUDA events inside the timed region, against
+           MEASURED_PEAKS.json hbm_gbs.
+`cpu_baseline`: the oracle (oracle/) on the host cores, rank 0 at N=1.
+`--impl reference`: the oracle as the reference arm (this tier has no
+           reference implementation).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+METRIC = "2.7K frame pairs/sec (disparity+point cloud) at 1/2/4/8 B200; HBM GB/s % peak"
+W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS = 2704, 1520, 4, 64, 5, 5
+WORKLOAD = ("C5 per GPU: stream of synthetic 2.7K RGB pairs, full pipeline a0-a8 "
+            "(prep s=4 -> BP 676x380 L=64 5 levels x 5 iters -> JBU r=2 to 2704x1520 -> reproject -> summary)")
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=60)
+    p.add_argument("--warmup", type=int, default=5)
+    p.add_argument("--batch", type=int, default=16, help="pairs per GPU per step")
+    p.add_argument("--pool", type=int, default=4, help="distinct synthetic pairs generated per rank")
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--cpu-threads", type=int, default=0)
+    return p.parse_args()
+
+
+# ----------------------------------------------------------------------------- helpers
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+    Q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.active,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.gpu = gpu_index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-i", str(self.gpu), "-lms", "100"], stdout=subprocess.PIPE,
+                                         stderr=subprocess.DEVNULL, text=True)
+        except (OSError, FileNotFoundError):
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return None
+        time.sleep(0.25)
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except subprocess.TimeoutExpired:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 7:
+                continue
+            try:
+                sm.append(float(f[0]))
+                mx.append(float(f[1]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[3:7]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        if not sm:
+            return None
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "samples": len(sm),
+                "reasons": sorted(reasons)}
+
+
+def make_pool(seed0: int, n: int):
+    import synthgen
+    lefts, rights = [], []
+    for i in range(n):
+        l, r, _ = synthgen.stereo_pair_rgb(seed0 + i, W_HI, H_HI, S_DOWN, 8, 48)
+        lefts.append(l)
+        rights.append(r)
+    return np.stack(lefts), np.stack(rights)
+
+
+def q_intrinsics():
+    import synthgen
+    I = synthgen.INTRINSICS
+    return I
+
+
+# ----------------------------------------------------------------------------- oracle timing
+def oracle_rate(n_threads: int, pairs_per_thread: int, left, right):
+    """Run the oracle pipeline (a0-a8) on n_threads host threads (ctypes releases the
+    GIL), each on pairs_per_thread pairs; returns (pairs/s, pairs, seconds)."""
+    import oracle
+    I = q_intrinsics()
+    Q = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+
+    def work(k):
+        for j in range(pairs_per_thread):
+            i = (k + j) % len(left)
+            oracle.pipeline_pair(left[i], right[i], S_DOWN, NDISP, LEVELS, ITERS, Q)
+
+    ts = [threading.Thread(target=work, args=(k,)) for k in range(n_threads)]
+    t0 = time.perf_counter()
+    for t in ts:
+        t.start()
+    for t in ts:
+        t.join()
+    dt = time.perf_counter() - t0
+    n = n_threads * pairs_per_thread
+    return n / dt, n, dt
+
+
+def default_threads():
+    try:
+        c = len(os.sched_getaffinity(0))
+    except AttributeError:
+        c = os.cpu_count() or 1
+    return max(1, min(c, 32))
+
+
+# ----------------------------------------------------------------------------- reference arm
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    import oracle
+    oracle.build()
+    threads = args.cpu_threads or default_threads()
+    left, right = make_pool(1000, min(args.pool, threads))
+    for _ in range(args.warmup):  # untimed rounds
+        oracle_rate(threads, 1, left, right)
+    times, pairs = 0.0, 0
+    for _ in range(args.steps):
+        _, n, dt = oracle_rate(threads, 1, left, right)
+        times += dt
+        pairs += n
+    v = pairs / times
+    line = {
+        "impl": "reference", "metric": METRIC, "value": v, "unit": "pairs/s", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000.0 * times / args.steps,
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
+        "data": "synthetic", "config": {"workload": WORKLOAD, "pairs_per_step": threads},
+        "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+                         "sample": f"{threads} pairs per step (one per host thread), {args.steps} steps"},
+        "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ----------------------------------------------------------------------------- our arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    import paper_1902_09733_b200 as P
+
+    rank, world, local = dist_env()
+    if world != args.gpus:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    P.lib()
+    B = args.batch
+    I = q_intrinsics()
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    pipe = P.StereoPipeline(W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS, batch=B, Q=Q, device=dev)
+    pipe.bp.timing(True)
+
+    # seeded synthetic pairs; rank r owns pairs i = r, r+N, ... (round-robin shard)
+    pool_n = max(1, min(args.pool, B))
+    lpool, rpool = make_pool(7000 + 100 * rank, pool_n)
+    idx = [i % pool_n for i in range(B)]
+    left_h = torch.from_numpy(lpool[idx]).pin_memory()
+    right_h = torch.from_numpy(rpool[idx]).pin_memory()
+    left_d = left_h.to(dev)
+    right_d = right_h.to(dev)
+    gathered = torch.empty((world * B, 8), dtype=torch.int64, device=dev)
+    stream = torch.cuda.current_stream(dev)
+
+    def step(s, lt, rt):
+        first = (s * world + rank) * B
+        summ = pipe.run(lt, rt, first_pair_id=first)
+        if world > 1:
+            dist.all_gather_into_tensor(gathered, summ)
+        else:
+            gathered.copy_(summ)
+        return summ
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+        torch.cuda.synchronize(dev)
+
+    def max_over_ranks(x: float) -> float:
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for s in range(args.warmup):
+        step(s, left_d, right_d)
+    pipe.bp.timing_read()  # discard warm-up timings
+    barrier()
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    n0 = P.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    e0.record(stream)
+    for s in range(args.steps):
+        step(args.warmup + s, left_d, right_d)
+    e1.record(stream)
+    barrier()
+    launches = P.launch_count() - n0
+    clocks = sampler.stop()
+    ms = e0.elapsed_time(e1)
+    ms_max = max_over_ranks(ms)
+    lv = pipe.bp.timing_read()
+    pairs = world * B * args.steps
+    value = pairs / (ms_max / 1000.0)
+
+    # ---- e2e: pinned host frames in, summaries out, through the public API
+    e2e = None
+    if not args.no_e2e:
+        summ_h = torch.empty((B, 8), dtype=torch.int64).pin_memory()
+        barrier()
+        f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        f0.record(stream)
+        for s in range(args.steps):
+            left_d.copy_(left_h, non_blocking=True)
+            right_d.copy_(right_h, non_blocking=True)
+            summ = step(args.warmup + args.steps + s, left_d, right_d)
+            summ_h.copy_(summ, non_blocking=True)
+        f1.record(stream)
+        barrier()
+        ems = max_over_ranks(f0.elapsed_time(f1))
+        e2e = {"value": pairs / (ems / 1000.0), "unit": "pairs/s",
+               "h2d_bytes_per_step": int(left_h.numel() + right_h.numel()),
+               "d2h_bytes_per_step": int(summ_h.numel() * 8)}
+        pipe.bp.timing_read()
+
+    # ---- roofline of the dominant kernel: level-0 message updates (a4)
+    peak, peak_kind = measured_peaks()
+    l0 = lv[0]
+    achieved = (l0["bytes"] / 1e9) / (l0["ms"] / 1e3) if l0["ms"] > 0 else 0.0
+    all_bytes = sum(x["bytes"] for x in lv)
+    all_ms = sum(x["ms"] for x in lv)
+    roofline = {
+        "kernel": "k_update (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
+        "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+        "traffic": None,
+        "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
+        "us_per_launch": 1000.0 * l0["ms"] / max(l0["launches"], 1),
+        "share_of_step": all_ms / (ms if ms > 0 else 1.0),
+        "all_levels_gbs": (all_bytes / 1e9) / (all_ms / 1e3) if all_ms > 0 else 0.0,
+    }
+
+    # ---- CPU baseline: the oracle on this host's cores (rank 0 at N=1 only)
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        threads = args.cpu_threads or default_threads()
+        v, n, dt = oracle_rate(threads, 1, lpool, rpool)
+        cpu = {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
+               "sample": f"{n} pairs of the same workload, one per host thread ({dt:.1f} s)"}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+            "config": {"workload": WORKLOAD, "batch_per_gpu": B, "pairs_per_step": world * B,
+                       "parallelism": f"dp{world} (pairs round-robin, NCCL all_gather of summaries)",
+                       "l2": f"inputs larger than L2 ({(left_d.numel() + right_d.numel()) / 1e6:.0f} MB RGB + "
+                             f"{pipe.bp.workspace.numel() / 1e6:.0f} MB BP state per step)",
+                       "bp_msg_storage": f"u{8 * pipe.bp.params()['msg_bytes']}",
+                       "jbu_arith": "f32"},
+            "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
+            "cpu_baseline": cpu,
+            "per_level_update_ms_per_step": [x["ms"] / args.steps for x in lv],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -1,0 +1,180 @@
+/*
+ * vsbp.h -- C ABI of the B200-native stereo hot path of arXiv 1902.09733
+ *           ("Towards Real-time 3D Reconstruction using Consumer UAVs").
+ *
+ * Library: paper_1902_09733_b200/libvsbp.so (sm_100a CUDA kernels + host glue).
+ * Citations: P:n = PAPER.md line n; R-n = reading n in DESIGN.md §3.
+ *
+ * Conventions for every entry point
+ *   - Buffer pointers are DEVICE pointers unless stated otherwise, owned by the
+ *     caller, row-major and tightly packed.  The library never allocates device
+ *     memory: scratch space is a caller-provided workspace (bp_set_workspace).
+ *   - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *     Every call only ENQUEUES work on that stream and never synchronises the
+ *     host; results are ready when the stream reaches that point.
+ *   - Return value: 0 on success, a negative VSBP_E* code on failure.  The
+ *     library never throws, aborts or prints; vsbp_strerror() describes a code
+ *     (for VSBP_ECUDA it carries the last CUDA error string of the calling thread).
+ *   - A context (vsbp_bp) may be used by one stream at a time; distinct contexts
+ *     are independent.
+ *   - There is no CPU implementation behind this ABI: without a B200 every
+ *     compute call returns VSBP_ECUDA.
+ */
+#ifndef VSBP_H
+#define VSBP_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VSBP_OK 0
+#define VSBP_EINVAL (-1)    /* null pointer, out-of-range size or parameter */
+#define VSBP_EDIM (-2)      /* dimension mismatch, workspace too small, batch > planned */
+#define VSBP_EOVERFLOW (-3) /* int32 fixed-point bound violated (see bp_create) */
+#define VSBP_ECUDA (-4)     /* CUDA launch/driver error (see vsbp_strerror) */
+
+typedef struct vsbp_bp vsbp_bp; /* opaque BP context */
+
+/* Per-pair summary written by pair_summary (a8): 64 bytes, device memory. */
+typedef struct vsbp_summary {
+    uint64_t n_valid;    /* points with d >= min_disp (reproject)              */
+    int64_t label_sum;   /* sum of low-res disparity labels                    */
+    uint64_t label_hash; /* sum_i mix64(i<<32 | label_i) mod 2^64  */
+    uint64_t pair_id;    /* caller's pair index                                */
+    uint64_t reserved[4];
+} vsbp_summary;
+
+/* ---------------------------------------------------------------------------
+ * bp_create -- plan hierarchical min-sum BP (§2.2 Eq.1, §3.2).
+ *   W, H      : BP resolution (the downsampled pair), W,H >= 1
+ *   ndisp     : number of labels L, disparities d in [0, L), 2 <= L <= 512
+ *   levels    : pyramid levels (1 = flat BP), 1 <= levels <= 16 (R-12)
+ *   iters     : checkerboard iterations per level (one iteration = one colour,
+ *               R-10), >= 1
+ *   lambda    : data-term weight (R-5), >= 0
+ *   data_trunc: truncation of |L - R| in intensity levels (R-2), rounds to >= 1
+ *   disc_trunc: smoothness truncation in labels (R-3), rounds to >= 1/128
+ * Fixed point (R-6): S = 128, lambda_q = rha(lambda*S), tau_d = rha(data_trunc),
+ * tau_q = rha(disc_trunc*S).
+ * Errors: VSBP_EINVAL for out-of-range arguments; VSBP_EOVERFLOW when
+ *   lambda_q*tau_d*4^(levels-1) + 4*tau_q + 2^20 >= 2^31 (R-25).
+ * Host-only; allocates only host metadata.  *out receives the context.
+ * ------------------------------------------------------------------------- */
+int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, float data_trunc,
+              float disc_trunc, vsbp_bp **out);
+
+/* Options (measurement / parity knobs); call before bp_set_workspace.
+ *   VSBP_OPT_MSG_BYTES : message storage width in bytes, 0 = narrowest lossless
+ *                        (u8 if tau_q <= 255, u16 if <= 65535, else 4), 1, 2 or 4;
+ *                        narrower than lossless -> VSBP_EINVAL.
+ *   VSBP_OPT_KERNEL    : 0 = fastest available message kernel, 1 = generic. */
+#define VSBP_OPT_MSG_BYTES 1
+#define VSBP_OPT_KERNEL 2
+int bp_set_option(vsbp_bp *ctx, int option, int value);
+
+/* Quantised parameters: out[0..7] = {lambda_q, tau_d, tau_q, S, msg_bytes,
+ * labels padded (Lp), levels, iters}. */
+int bp_get_params(const vsbp_bp *ctx, int32_t out[8]);
+
+/* Dimensions of pyramid level `level` (ceil-halving, R-12). */
+int bp_level_dims(const vsbp_bp *ctx, int level, int *W, int *H);
+
+/* Device scratch needed for `batch` pairs, and binding it (caller-owned,
+ * 256-byte aligned, must outlive every call that uses it). */
+size_t bp_workspace_bytes(const vsbp_bp *ctx, int batch);
+int bp_set_workspace(vsbp_bp *ctx, void *dptr, size_t bytes, int batch);
+
+/* ---------------------------------------------------------------------------
+ * bp_disparity_batch -- a1..a5 for B independent pairs.
+ *   left, right : u8 [B][H][W] rectified, downsampled grey pairs
+ *   disp        : int32 [B][H][W] labels, the WTA argmin of Eq.1's E_X(d)
+ *                 (P:34), ties -> smallest d (R-13)
+ * Requires a workspace bound for >= B pairs (else VSBP_EDIM).
+ * The per-level message fields stay in the workspace for bp_get_messages.
+ * bp_disparity is the B = 1 case.
+ * ------------------------------------------------------------------------- */
+int bp_disparity_batch(vsbp_bp *ctx, int B, const uint8_t *left, const uint8_t *right, int32_t *disp,
+                       void *stream);
+int bp_disparity(vsbp_bp *ctx, const uint8_t *left, const uint8_t *right, int32_t *disp, void *stream);
+
+/* Debug / parity export after bp_disparity*: the final messages of `level` for
+ * pair `pair`, as int32 [4][H_l][W_l][L] with M[k][y][x][d] = message pixel
+ * (x,y) sends toward direction k (0 up, 1 down, 2 left, 3 right); and the cost
+ * pyramid level as int32 [H_l][W_l][L]. */
+int bp_get_messages(vsbp_bp *ctx, int pair, int level, int32_t *out, void *stream);
+int bp_get_costs(vsbp_bp *ctx, int pair, int level, int32_t *out, void *stream);
+
+void bp_destroy(vsbp_bp *ctx);
+
+/* ---------------------------------------------------------------------------
+ * jbu_upsample_batch -- a6, joint bilateral upsampling (Eq.2; R-15..R-19,
+ * R-24).  For B pairs:
+ *   disp_lo   : int32 [B][H][W] low-res labels
+ *   guide_rgb : u8 [B][s*H][s*W][3] full-res colour guide (the left frame, R-17)
+ *   disp_hi   : float [B][s*H][s*W] upsampled disparity in FULL-RES pixels (x s)
+ *   sigma_s   : spatial sigma in LOW-RES pixels (> 0); sigma_r: range sigma on
+ *               the 0..255 scale (> 0); radius: window half-width in low-res
+ *               pixels, 1..8; s: integer scale 1..16.
+ * f32 arithmetic; agrees with the double oracle within 1e-4 full-res px.
+ * jbu_upsample is the B = 1 case.
+ * ------------------------------------------------------------------------- */
+int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s,
+                       float *disp_hi, float sigma_s, float sigma_r, int radius, void *stream);
+int jbu_upsample(const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
+                 float sigma_s, float sigma_r, int radius, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * reproject_batch -- a7, Eq.3 (R-20, R-21):
+ *   [X Y Z Wh]^T = Q [u v d 1]^T, xyz = (X,Y,Z)/Wh if d >= min_disp else NaN.
+ *   disp    : float [B][H][W] full-res disparity (px)
+ *   Q       : HOST pointer, double[16] row-major (copied at call time)
+ *   xyz     : float [B][H][W][3]
+ *   n_valid : device uint64 [B]; overwritten with the count of valid points.
+ * min_disp <= 0 -> VSBP_EINVAL.  reproject is the B = 1 case.
+ * ------------------------------------------------------------------------- */
+int reproject_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+                    unsigned long long *n_valid, void *stream);
+int reproject(const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+              unsigned long long *n_valid, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * prep_downsample_batch -- a0 (R-22): for n frames,
+ *   rgb_hi : u8 [n][H_hi][W_hi][3]  ->  gray_lo : u8 [n][H_hi/s][W_hi/s]
+ *   grey = (77R+150G+29B+128)>>8, then s x s mean rounded half up.
+ * W_hi, H_hi must be multiples of s (else VSBP_EDIM).
+ * ------------------------------------------------------------------------- */
+int prep_downsample_batch(int n, const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *gray_lo,
+                          void *stream);
+int prep_downsample(const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *gray_lo, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * pair_summary_batch -- a8: for B pairs write summary[b] =
+ *   {n_valid[b], sum of disp_lo[b], label hash of disp_lo[b], first_pair_id + b}.
+ *   disp_lo : int32 [B][H][W]; n_valid : device uint64 [B]; summary : device [B].
+ * ------------------------------------------------------------------------- */
+int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsigned long long *n_valid,
+                       uint64_t first_pair_id, vsbp_summary *summary, void *stream);
+
+/* Live timing of the message-update kernels (a4), for bench.py's roofline.
+ * bp_timing_enable(ctx, 1) makes every later bp_disparity* record CUDA events
+ * (on the call's stream) around each level's run of update launches;
+ * bp_timing_read synchronises those events and returns, accumulated since the
+ * last read, per level l < 16: ms[l] = device milliseconds of the level's update
+ * launches, launches[l] = number of launches, bytes[l] = their ALGORITHMIC bytes
+ * (updated pixels x (L*w_D + 8*L*w_M)).  Host pointers, >= 16 entries. */
+int bp_timing_enable(vsbp_bp *ctx, int enable);
+int bp_timing_read(vsbp_bp *ctx, double *ms, int64_t *launches, double *bytes);
+
+const char *vsbp_strerror(int code);
+
+/* Number of kernel launches this thread has enqueued through the library
+ * (monotone counter; bench.py reports the difference over the timed region). */
+uint64_t vsbp_launch_count(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* VSBP_H */

@@ -347,8 +347,10 @@ int oracle_bp_disparity(const uint8_t *left, const uint8_t *right, int W, int H,
     int rc = oracle_quantize(lambda, data_trunc, disc_trunc, q);
     if (rc) return rc;
     int32_t lam_q = q[0], tau_d = q[1], tau_q = q[2], S = q[3];
-    /* int32 bound (R-12 / O5): the largest belief at the top level must fit */
-    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q;
+    /* int32 bound (O5, R-25): the largest belief at the top level plus
+     * 2^20 of headroom for the distance transform's additions must fit */
+    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q +
+                    ((int64_t)1 << 20);
     if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
 
     int Ws[16], Hs[16];

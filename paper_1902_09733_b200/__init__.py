@@ -1,0 +1,306 @@
+"""B200-native stereo hot path of arXiv 1902.09733 -- Python binding.
+
+Thin ctypes marshalling over ``libvsbp.so`` (C ABI: ``include/vsbp.h``).  Torch is
+used only for device memory and streams; every step of the path runs in the
+library's sm_100a kernels.  There is no CPU fallback: if the library is missing
+or a call fails, this module raises.
+
+Entry points mirror the C ABI (names follow the paper's steps):
+  StereoBP(W, H, ndisp, levels, iters, lam, data_trunc, disc_trunc)  -- bp_create
+      .disparity(left, right)                                        -- bp_disparity_batch (a1-a5)
+      .messages(pair, level) / .costs(pair, level)                   -- parity exports
+  jbu_upsample(disp_lo, guide_rgb, s, sigma_s, sigma_r, radius)      -- a6 (Eq.2)
+  reproject(disp, Q, min_disp)                                       -- a7 (Eq.3)
+  prep_downsample(rgb, s)                                            -- a0
+  pair_summary(disp_lo, n_valid, first_pair_id)                      -- a8
+  StereoPipeline                                                     -- a0-a8 for a batch of pairs
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+import torch
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libvsbp.so")
+
+VSBP_OPT_MSG_BYTES = 1
+VSBP_OPT_KERNEL = 2
+_ERRNAMES = {-1: "VSBP_EINVAL", -2: "VSBP_EDIM", -3: "VSBP_EOVERFLOW", -4: "VSBP_ECUDA"}
+
+
+class VsbpError(RuntimeError):
+    def __init__(self, code: int, fn: str, msg: str):
+        super().__init__(f"{fn}: {_ERRNAMES.get(code, code)} ({msg})")
+        self.code = code
+
+
+_lib = None
+_EXPORTS = {
+    # name: (restype, argtypes)
+    "bp_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float, C.c_float,
+                            C.POINTER(C.c_void_p)]),
+    "bp_set_option": (C.c_int, [C.c_void_p, C.c_int, C.c_int]),
+    "bp_get_params": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "bp_level_dims": (C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "bp_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int]),
+    "bp_set_workspace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
+    "bp_disparity_batch": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "bp_disparity": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "bp_get_messages": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "bp_get_costs": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "bp_destroy": (None, [C.c_void_p]),
+    "jbu_upsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                     C.c_float, C.c_float, C.c_int, C.c_void_p]),
+    "jbu_upsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_float,
+                               C.c_float, C.c_int, C.c_void_p]),
+    "reproject_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p,
+                                  C.c_void_p, C.c_void_p]),
+    "reproject": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
+                            C.c_void_p]),
+    "prep_downsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
+                                        C.c_void_p]),
+    "prep_downsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "pair_summary_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
+                                     C.c_void_p, C.c_void_p]),
+    "bp_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
+    "bp_timing_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vsbp_strerror": (C.c_char_p, [C.c_int]),
+    "vsbp_launch_count": (C.c_uint64, []),
+}
+
+
+def lib():
+    """Load libvsbp.so (built in-tree by ``__graft_entry__.build()``); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"{LIB_PATH} is not built; run `python -c 'import __graft_entry__ as g; g.build()'`. "
+                               "There is no CPU fallback.")
+        L = C.CDLL(LIB_PATH)
+        for name, (res, args) in _EXPORTS.items():
+            fn = getattr(L, name)
+            fn.restype = res
+            fn.argtypes = args
+        _lib = L
+    return _lib
+
+
+def _check(rc: int, fn: str):
+    if rc != 0:
+        raise VsbpError(rc, fn, lib().vsbp_strerror(rc).decode())
+
+
+def _stream(stream=None) -> C.c_void_p:
+    s = torch.cuda.current_stream() if stream is None else stream
+    return C.c_void_p(s.cuda_stream)
+
+
+def _dev(t: torch.Tensor, dtype, name: str) -> C.c_void_p:
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError(f"{name} must be a CUDA tensor")
+    if t.dtype != dtype:
+        raise TypeError(f"{name} must be {dtype}, got {t.dtype}")
+    if not t.is_contiguous():
+        raise ValueError(f"{name} must be contiguous")
+    return C.c_void_p(t.data_ptr())
+
+
+def launch_count() -> int:
+    return int(lib().vsbp_launch_count())
+
+
+# ----------------------------------------------------------------------------- BP
+class StereoBP:
+    """Hierarchical checkerboard min-sum BP (Eq.1), a1-a5.  Owns its
+    device workspace (a torch uint8 tensor) for up to ``batch`` pairs."""
+
+    def __init__(self, W, H, ndisp, levels, iters, lam=0.07, data_trunc=15.0, disc_trunc=1.7, batch=1,
+                 msg_bytes=0, kernel=0, device="cuda"):
+        self._h = C.c_void_p()
+        _check(lib().bp_create(W, H, ndisp, levels, iters, lam, data_trunc, disc_trunc, C.byref(self._h)),
+               "bp_create")
+        if msg_bytes:
+            _check(lib().bp_set_option(self._h, VSBP_OPT_MSG_BYTES, msg_bytes), "bp_set_option")
+        if kernel:
+            _check(lib().bp_set_option(self._h, VSBP_OPT_KERNEL, kernel), "bp_set_option")
+        self.W, self.H, self.L, self.levels, self.iters, self.batch = W, H, ndisp, levels, iters, batch
+        nbytes = int(lib().bp_workspace_bytes(self._h, batch))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _check(lib().bp_set_workspace(self._h, C.c_void_p(self.workspace.data_ptr()), nbytes, batch),
+               "bp_set_workspace")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.bp_destroy(h)
+            self._h = None
+
+    def params(self) -> dict:
+        out = (C.c_int32 * 8)()
+        _check(lib().bp_get_params(self._h, out), "bp_get_params")
+        keys = ["lam_q", "tau_d", "tau_q", "S", "msg_bytes", "Lp", "levels", "iters"]
+        return dict(zip(keys, [int(v) for v in out]))
+
+    def level_dims(self, level: int):
+        w, h = C.c_int(), C.c_int()
+        _check(lib().bp_level_dims(self._h, level, C.byref(w), C.byref(h)), "bp_level_dims")
+        return w.value, h.value
+
+    def disparity(self, left: torch.Tensor, right: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        """left, right: uint8 [B,H,W] (or [H,W]) -> int32 labels of the same shape."""
+        squeeze = left.dim() == 2
+        if squeeze:
+            left, right = left.unsqueeze(0), right.unsqueeze(0)
+        B = left.shape[0]
+        if tuple(left.shape) != (B, self.H, self.W) or tuple(right.shape) != (B, self.H, self.W):
+            raise ValueError(f"expected [B,{self.H},{self.W}] images, got {tuple(left.shape)}, {tuple(right.shape)}")
+        if out is None:
+            out = torch.empty((B, self.H, self.W), dtype=torch.int32, device=left.device)
+        _check(lib().bp_disparity_batch(self._h, B, _dev(left, torch.uint8, "left"),
+                                        _dev(right, torch.uint8, "right"), _dev(out, torch.int32, "disp"),
+                                        _stream(stream)), "bp_disparity_batch")
+        return out[0] if squeeze else out
+
+    def messages(self, pair: int, level: int, stream=None) -> torch.Tensor:
+        w, h = self.level_dims(level)
+        out = torch.empty((4, h, w, self.L), dtype=torch.int32, device=self.workspace.device)
+        _check(lib().bp_get_messages(self._h, pair, level, _dev(out, torch.int32, "out"), _stream(stream)),
+               "bp_get_messages")
+        return out
+
+    def timing(self, enable: bool = True):
+        _check(lib().bp_timing_enable(self._h, 1 if enable else 0), "bp_timing_enable")
+
+    def timing_read(self):
+        """Accumulated (since the last read) per-level device ms, launches and
+        algorithmic bytes of the message-update kernels."""
+        ms = (C.c_double * 16)()
+        n = (C.c_int64 * 16)()
+        by = (C.c_double * 16)()
+        _check(lib().bp_timing_read(self._h, ms, n, by), "bp_timing_read")
+        return [dict(level=l, ms=ms[l], launches=int(n[l]), bytes=by[l]) for l in range(self.levels)]
+
+    def costs(self, pair: int, level: int, stream=None) -> torch.Tensor:
+        w, h = self.level_dims(level)
+        out = torch.empty((h, w, self.L), dtype=torch.int32, device=self.workspace.device)
+        _check(lib().bp_get_costs(self._h, pair, level, _dev(out, torch.int32, "out"), _stream(stream)),
+               "bp_get_costs")
+        return out
+
+
+# ----------------------------------------------------------------------------- a0, a6, a7, a8
+def prep_downsample(rgb: torch.Tensor, s: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """rgb: uint8 [n,H,W,3] (or [H,W,3]) -> grey box-downsampled uint8 [n,H/s,W/s]."""
+    squeeze = rgb.dim() == 3
+    if squeeze:
+        rgb = rgb.unsqueeze(0)
+    n, H, W, _ = rgb.shape
+    if out is None:
+        out = torch.empty((n, H // s, W // s), dtype=torch.uint8, device=rgb.device)
+    _check(lib().prep_downsample_batch(n, _dev(rgb, torch.uint8, "rgb"), W, H, s, _dev(out, torch.uint8, "gray"),
+                                       _stream(stream)), "prep_downsample_batch")
+    return out[0] if squeeze else out
+
+
+def jbu_upsample(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_s: float, sigma_r: float,
+                 radius: int, out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """disp_lo int32 [B,H,W], guide uint8 [B,sH,sW,3] -> float32 [B,sH,sW] (full-res px)."""
+    squeeze = disp_lo.dim() == 2
+    if squeeze:
+        disp_lo, guide_rgb = disp_lo.unsqueeze(0), guide_rgb.unsqueeze(0)
+    B, H, W = disp_lo.shape
+    if tuple(guide_rgb.shape) != (B, H * s, W * s, 3):
+        raise ValueError("guide must be [B, s*H, s*W, 3]")
+    if out is None:
+        out = torch.empty((B, H * s, W * s), dtype=torch.float32, device=disp_lo.device)
+    _check(lib().jbu_upsample_batch(B, _dev(disp_lo, torch.int32, "disp_lo"), W, H,
+                                    _dev(guide_rgb, torch.uint8, "guide_rgb"), s, _dev(out, torch.float32, "disp_hi"),
+                                    sigma_s, sigma_r, radius, _stream(stream)), "jbu_upsample_batch")
+    return out[0] if squeeze else out
+
+
+def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.ndarray:
+    """Eq.3 as a 4x4 reprojection matrix with z = f B/(d du) (R-20)."""
+    return np.array([[1.0, 0.0, 0.0, -u0],
+                     [0.0, f_du / f_dv, 0.0, -v0 * f_du / f_dv],
+                     [0.0, 0.0, 0.0, f_du],
+                     [0.0, 0.0, 1.0 / B, 0.0]], dtype=np.float64)
+
+
+def reproject(disp: torch.Tensor, Q, min_disp: float = 1.0, xyz: torch.Tensor | None = None,
+              n_valid: torch.Tensor | None = None, stream=None):
+    """disp float32 [B,H,W] -> (xyz float32 [B,H,W,3], n_valid int64 [B])."""
+    squeeze = disp.dim() == 2
+    if squeeze:
+        disp = disp.unsqueeze(0)
+    B, H, W = disp.shape
+    Qh = np.ascontiguousarray(np.asarray(Q, np.float64).reshape(16))
+    if xyz is None:
+        xyz = torch.empty((B, H, W, 3), dtype=torch.float32, device=disp.device)
+    if n_valid is None:
+        n_valid = torch.empty(B, dtype=torch.int64, device=disp.device)
+    _check(lib().reproject_batch(B, _dev(disp, torch.float32, "disp"), W, H, Qh.ctypes.data_as(C.c_void_p),
+                                 min_disp, _dev(xyz, torch.float32, "xyz"), _dev(n_valid, torch.int64, "n_valid"),
+                                 _stream(stream)), "reproject_batch")
+    if squeeze:
+        return xyz[0], n_valid
+    return xyz, n_valid
+
+
+SUMMARY_BYTES = 64
+
+
+def pair_summary(disp_lo: torch.Tensor, n_valid: torch.Tensor, first_pair_id: int = 0,
+                 out: torch.Tensor | None = None, stream=None) -> torch.Tensor:
+    """a8: int64 [B,8] rows {n_valid, label_sum, label_hash (as int64 bits), pair_id, 0,0,0,0}."""
+    if disp_lo.dim() == 2:
+        disp_lo = disp_lo.unsqueeze(0)
+    B, H, W = disp_lo.shape
+    if out is None:
+        out = torch.empty((B, 8), dtype=torch.int64, device=disp_lo.device)
+    _check(lib().pair_summary_batch(B, _dev(disp_lo, torch.int32, "disp_lo"), W, H,
+                                    _dev(n_valid, torch.int64, "n_valid"), first_pair_id,
+                                    _dev(out, torch.int64, "summary"), _stream(stream)), "pair_summary_batch")
+    return out
+
+
+# ----------------------------------------------------------------------------- a0-a8
+class StereoPipeline:
+    """The whole hot path for batches of B 2.7K RGB pairs (a0-a8), all on one
+    stream: prep both frames, hierarchical BP, JBU (guide = left frame),
+    reprojection, per-pair summary.  Buffers are allocated once."""
+
+    def __init__(self, W_hi, H_hi, s, ndisp, levels, iters, batch, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
+                 sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0):
+        self.W_hi, self.H_hi, self.s, self.B = W_hi, H_hi, s, batch
+        self.W, self.H = W_hi // s, H_hi // s
+        self.sigma_s = 15.0 / s if sigma_s is None else sigma_s  # R-16
+        self.sigma_r = sigma_r
+        self.radius = -(-5 // s) if radius is None else radius
+        self.min_disp = min_disp
+        self.Q = Q
+        self.bp = StereoBP(self.W, self.H, ndisp, levels, iters, lam, data_trunc, disc_trunc, batch=batch,
+                           msg_bytes=msg_bytes, device=device)
+        dev = torch.device(device)
+        self.gray = torch.empty((2, batch, self.H, self.W), dtype=torch.uint8, device=dev)
+        self.disp = torch.empty((batch, self.H, self.W), dtype=torch.int32, device=dev)
+        self.disp_hi = torch.empty((batch, H_hi, W_hi), dtype=torch.float32, device=dev)
+        self.xyz = torch.empty((batch, H_hi, W_hi, 3), dtype=torch.float32, device=dev)
+        self.n_valid = torch.zeros(batch, dtype=torch.int64, device=dev)
+        self.summary = torch.empty((batch, 8), dtype=torch.int64, device=dev)
+
+    def run(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, first_pair_id: int = 0, stream=None):
+        """left_rgb, right_rgb: uint8 [B,H_hi,W_hi,3] on the device.  Returns the
+        per-pair summary tensor (device); disp / disp_hi / xyz stay in the object."""
+        B = left_rgb.shape[0]
+        prep_downsample(left_rgb, self.s, out=self.gray[0, :B], stream=stream)
+        prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
+        self.bp.disparity(self.gray[0, :B], self.gray[1, :B], out=self.disp[:B], stream=stream)
+        jbu_upsample(self.disp[:B], left_rgb, self.s, self.sigma_s, self.sigma_r, self.radius,
+                     out=self.disp_hi[:B], stream=stream)
+        reproject(self.disp_hi[:B], self.Q, self.min_disp, xyz=self.xyz[:B], n_valid=self.n_valid[:B],
+                  stream=stream)
+        return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=self.summary[:B], stream=stream)

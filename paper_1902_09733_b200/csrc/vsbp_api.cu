@@ -1,0 +1,435 @@
+// vsbp_api.cu -- the C ABI (include/vsbp.h): context, parameter quantisation,
+// workspace plan and the launch sequence of hierarchical BP (SURVEY §3 call
+// stacks).  Host code only; every device step is a kernel in bp_kernels.cu or
+// pipeline_kernels.cu.
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <new>
+
+#include "vsbp.h"
+#include "vsbp_internal.cuh"
+#include "vsbp_kernels.h"
+
+struct vsbp_bp {
+    int W, H, L, levels, iters;
+    int lam_q, tau_d, tau_q, S;
+    int Lp, nch, G, log2G;
+    int msg_bytes_opt, msg_bytes, kernel;
+    int Wl[16], Hl[16], Wcl[16];
+    int dbytes[16];
+    // workspace plan (bytes) for ws_batch pairs
+    size_t d_off[16], m_off[16], total;
+    void *ws;
+    size_t ws_bytes;
+    int ws_batch;
+    int last_B;
+    // live timing of the a4 launches (bp_timing_enable)
+    int timing;
+    int n_pending;
+    cudaEvent_t ev[64][2];
+    int ev_level[64];
+    int ev_launches[64];
+    double ev_bytes[64];
+    double acc_ms[16], acc_bytes[16];
+    int64_t acc_launches[16];
+};
+
+namespace {
+
+thread_local char g_errbuf[256];
+thread_local uint64_t g_launches;
+
+int cuda_fail(cudaError_t e)
+{
+    snprintf(g_errbuf, sizeof g_errbuf, "CUDA error: %s", cudaGetErrorString(e));
+    return VSBP_ECUDA;
+}
+
+#define CK(expr)                                  \
+    do {                                          \
+        cudaError_t e_ = (expr);                  \
+        if (e_ != cudaSuccess) return cuda_fail(e_); \
+    } while (0)
+
+long long rha(double v) { return v >= 0 ? (long long)std::floor(v + 0.5) : -(long long)std::floor(-v + 0.5); }
+
+int bytes_for_max(long long vmax)
+{
+    if (vmax <= 255) return 1;
+    if (vmax <= 65535) return 2;
+    return 4;
+}
+
+size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
+
+void plan(vsbp_bp *c, int batch)
+{
+    size_t off = 0;
+    for (int l = 0; l < c->levels; ++l) {
+        c->d_off[l] = off;
+        off = align256(off + (size_t)batch * 2 * c->Hl[l] * c->Wcl[l] * c->Lp * c->dbytes[l]);
+    }
+    for (int l = 0; l < c->levels; ++l) {
+        c->m_off[l] = off;
+        off = align256(off + (size_t)batch * 8 * c->Hl[l] * c->Wcl[l] * c->Lp * c->msg_bytes);
+    }
+    c->total = off;
+}
+
+vsbp::Geom geom(const vsbp_bp *c, int B, int l)
+{
+    vsbp::Geom g;
+    g.B = B;
+    g.W = c->Wl[l];
+    g.H = c->Hl[l];
+    g.Wc = c->Wcl[l];
+    const int lp = l + 1 < c->levels ? l + 1 : l;
+    g.Wp = c->Wl[lp];
+    g.Hp = c->Hl[lp];
+    g.Wcp = c->Wcl[lp];
+    g.L = c->L;
+    g.Lp = c->Lp;
+    g.nch = c->nch;
+    g.G = c->G;
+    g.log2G = c->log2G;
+    return g;
+}
+
+inline char *wsp(const vsbp_bp *c) { return (char *)c->ws; }
+
+}  // namespace
+
+namespace vsbp {
+void note_launch(int n) { g_launches += (uint64_t)n; }
+}  // namespace vsbp
+
+static int timing_drain(vsbp_bp *c)
+{
+    for (int i = 0; i < c->n_pending; ++i) {
+        float ms = 0.f;
+        CK(cudaEventSynchronize(c->ev[i][1]));
+        CK(cudaEventElapsedTime(&ms, c->ev[i][0], c->ev[i][1]));
+        const int l = c->ev_level[i];
+        c->acc_ms[l] += ms;
+        c->acc_launches[l] += c->ev_launches[i];
+        c->acc_bytes[l] += c->ev_bytes[i];
+    }
+    c->n_pending = 0;
+    return VSBP_OK;
+}
+
+extern "C" {
+
+uint64_t vsbp_launch_count(void) { return g_launches; }
+
+const char *vsbp_strerror(int code)
+{
+    switch (code) {
+    case VSBP_OK: return "ok";
+    case VSBP_EINVAL: return "invalid argument";
+    case VSBP_EDIM: return "dimension mismatch or workspace too small";
+    case VSBP_EOVERFLOW: return "int32 fixed-point bound exceeded";
+    case VSBP_ECUDA: return g_errbuf[0] ? g_errbuf : "CUDA error";
+    default: return "unknown error";
+    }
+}
+
+int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, float data_trunc, float disc_trunc,
+              vsbp_bp **out)
+{
+    if (!out || W < 1 || H < 1 || ndisp < 2 || ndisp > 512 || levels < 1 || levels > 16 || iters < 1)
+        return VSBP_EINVAL;
+    if (!(lambda >= 0.0f) || !(data_trunc > 0.0f) || !(disc_trunc > 0.0f)) return VSBP_EINVAL;
+    if ((long long)W * H > (1ll << 28)) return VSBP_EINVAL;
+    const double S = 128.0;  // 2^7, R-6
+    const long long lq = rha((double)lambda * S), td = rha((double)data_trunc), tq = rha((double)disc_trunc * S);
+    if (td < 1 || tq < 1) return VSBP_EINVAL;
+    // R-25: beliefs plus the DT's carry headroom (2^20) must stay below 2^31
+    const double bound = (double)lq * (double)td * std::ldexp(1.0, 2 * (levels - 1)) + 4.0 * (double)tq + 1048576.0;
+    if (bound >= 2147483648.0) return VSBP_EOVERFLOW;
+    vsbp_bp *c = new (std::nothrow) vsbp_bp;
+    if (!c) return VSBP_EINVAL;
+    memset(c, 0, sizeof *c);
+    c->W = W;
+    c->H = H;
+    c->L = ndisp;
+    c->levels = levels;
+    c->iters = iters;
+    c->lam_q = (int)lq;
+    c->tau_d = (int)td;
+    c->tau_q = (int)tq;
+    c->S = (int)S;
+    c->Lp = (ndisp + vsbp::CH - 1) / vsbp::CH * vsbp::CH;
+    c->nch = c->Lp / vsbp::CH;
+    c->G = 1;
+    c->log2G = 0;
+    while (c->G < c->nch) {
+        c->G <<= 1;
+        c->log2G++;
+    }
+    int w = W, h = H;
+    for (int l = 0; l < levels; ++l) {
+        c->Wl[l] = w;
+        c->Hl[l] = h;
+        c->Wcl[l] = (w + 1) / 2;
+        c->dbytes[l] = bytes_for_max((long long)c->lam_q * c->tau_d << (2 * l));
+        w = (w + 1) / 2;
+        h = (h + 1) / 2;
+    }
+    c->msg_bytes = bytes_for_max(c->tau_q);
+    *out = c;
+    return VSBP_OK;
+}
+
+int bp_set_option(vsbp_bp *c, int option, int value)
+{
+    if (!c) return VSBP_EINVAL;
+    if (option == VSBP_OPT_MSG_BYTES) {
+        const int lossless = bytes_for_max(c->tau_q);
+        if (value == 0) value = lossless;
+        if (value != 1 && value != 2 && value != 4) return VSBP_EINVAL;
+        if (value < lossless) return VSBP_EINVAL;
+        c->msg_bytes = value;
+        c->ws = nullptr;  // plan changes: workspace must be re-bound
+        c->ws_batch = 0;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_KERNEL) {
+        if (value < 0 || value > 1) return VSBP_EINVAL;
+        c->kernel = value;
+        return VSBP_OK;
+    }
+    return VSBP_EINVAL;
+}
+
+int bp_get_params(const vsbp_bp *c, int32_t out[8])
+{
+    if (!c || !out) return VSBP_EINVAL;
+    out[0] = c->lam_q;
+    out[1] = c->tau_d;
+    out[2] = c->tau_q;
+    out[3] = c->S;
+    out[4] = c->msg_bytes;
+    out[5] = c->Lp;
+    out[6] = c->levels;
+    out[7] = c->iters;
+    return VSBP_OK;
+}
+
+int bp_level_dims(const vsbp_bp *c, int level, int *W, int *H)
+{
+    if (!c || !W || !H || level < 0 || level >= c->levels) return VSBP_EINVAL;
+    *W = c->Wl[level];
+    *H = c->Hl[level];
+    return VSBP_OK;
+}
+
+size_t bp_workspace_bytes(const vsbp_bp *c, int batch)
+{
+    if (!c || batch < 1) return 0;
+    vsbp_bp tmp = *c;
+    plan(&tmp, batch);
+    return tmp.total;
+}
+
+int bp_set_workspace(vsbp_bp *c, void *dptr, size_t bytes, int batch)
+{
+    if (!c || !dptr || batch < 1) return VSBP_EINVAL;
+    if (((uintptr_t)dptr & 255) != 0) return VSBP_EINVAL;
+    plan(c, batch);
+    if (bytes < c->total) return VSBP_EDIM;
+    c->ws = dptr;
+    c->ws_bytes = bytes;
+    c->ws_batch = batch;
+    return VSBP_OK;
+}
+
+int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *right, int32_t *disp, void *stream)
+{
+    if (!c || !left || !right || !disp || B < 1) return VSBP_EINVAL;
+    if (!c->ws || B > c->ws_batch) return VSBP_EDIM;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (c->timing && c->n_pending + c->levels > 64) {
+        int rc = timing_drain(c);
+        if (rc) return rc;
+    }
+    // the workspace is planned for ws_batch pairs: level arrays are [ws_batch][...],
+    // a call with B <= ws_batch uses the first B slots (offsets are per-level bases)
+    plan(c, c->ws_batch);
+    char *ws = wsp(c);
+    const int top = c->levels - 1;
+    // a1: cost volume, a2: pyramid
+    {
+        vsbp::Geom g = geom(c, B, 0);
+        CK(vsbp::launch_costvol(left, right, ws + c->d_off[0], c->dbytes[0], g, c->lam_q, c->tau_d, st));
+    }
+    for (int l = 0; l < top; ++l) {
+        vsbp::Geom g = geom(c, B, l);
+        CK(vsbp::launch_pyramid(ws + c->d_off[l], c->dbytes[l], ws + c->d_off[l + 1], c->dbytes[l + 1], g, st));
+    }
+    // a3 + a4, coarse to fine
+    for (int l = top; l >= 0; --l) {
+        vsbp::Geom g = geom(c, B, l);
+        void *D = ws + c->d_off[l];
+        void *M = ws + c->m_off[l];
+        const void *Mp = (l < top) ? (const void *)(ws + c->m_off[l + 1]) : nullptr;
+        if (c->iters == 1) {
+            // colour 1 is never updated on this level: materialise its initial
+            // messages (0 at the top, the parent's otherwise), R-12
+            if (l == top) {
+                for (int b = 0; b < B; ++b)
+                    CK(cudaMemsetAsync(ws + c->m_off[l] + (size_t)b * 8 * g.H * g.Wc * g.Lp * c->msg_bytes, 0,
+                                       (size_t)8 * g.H * g.Wc * g.Lp * c->msg_bytes, st));
+            } else {
+                CK(vsbp::launch_upcopy(M, Mp, c->msg_bytes, g, 1, st));
+            }
+        }
+        const int slot = (c->timing && c->n_pending < 64) ? c->n_pending++ : -1;
+        if (slot >= 0) CK(cudaEventRecord(c->ev[slot][0], st));
+        double bytes = 0.0;
+        for (int t = 0; t < c->iters; ++t) {
+            const int mode = (t > 0) ? 0 : (l == top ? 1 : 2);
+            CK(vsbp::launch_update(D, c->dbytes[l], M, Mp, c->msg_bytes, g, mode, t & 1, c->S, c->tau_q, st));
+            // pixels of colour t&1: ceil/floor split of each row
+            long long npix = 0;
+            for (int y = 0; y < g.H; ++y) npix += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;
+            bytes += (double)B * npix * ((double)c->L * c->dbytes[l] + 8.0 * c->L * c->msg_bytes);
+        }
+        if (slot >= 0) {
+            CK(cudaEventRecord(c->ev[slot][1], st));
+            c->ev_level[slot] = l;
+            c->ev_launches[slot] = c->iters;
+            c->ev_bytes[slot] = bytes;
+        }
+    }
+    // a5
+    {
+        vsbp::Geom g = geom(c, B, 0);
+        CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, st));
+    }
+    c->last_B = B;
+    return VSBP_OK;
+}
+
+int bp_disparity(vsbp_bp *c, const uint8_t *left, const uint8_t *right, int32_t *disp, void *stream)
+{
+    return bp_disparity_batch(c, 1, left, right, disp, stream);
+}
+
+int bp_get_messages(vsbp_bp *c, int pair, int level, int32_t *out, void *stream)
+{
+    if (!c || !out || level < 0 || level >= c->levels || pair < 0) return VSBP_EINVAL;
+    if (!c->ws || pair >= c->ws_batch) return VSBP_EDIM;
+    plan(c, c->ws_batch);
+    vsbp::Geom g = geom(c, c->ws_batch, level);
+    CK(vsbp::launch_export_msgs(wsp(c) + c->m_off[level], c->msg_bytes, g, pair, out, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int bp_get_costs(vsbp_bp *c, int pair, int level, int32_t *out, void *stream)
+{
+    if (!c || !out || level < 0 || level >= c->levels || pair < 0) return VSBP_EINVAL;
+    if (!c->ws || pair >= c->ws_batch) return VSBP_EDIM;
+    plan(c, c->ws_batch);
+    vsbp::Geom g = geom(c, c->ws_batch, level);
+    CK(vsbp::launch_export_costs(wsp(c) + c->d_off[level], c->dbytes[level], g, pair, out, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int bp_timing_enable(vsbp_bp *c, int enable)
+{
+    if (!c) return VSBP_EINVAL;
+    if (enable && !c->timing) {
+        for (int i = 0; i < 64; ++i)
+            for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&c->ev[i][j]));
+    }
+    if (!enable && c->timing) {
+        for (int i = 0; i < 64; ++i)
+            for (int j = 0; j < 2; ++j) cudaEventDestroy(c->ev[i][j]);
+        c->n_pending = 0;
+    }
+    c->timing = enable ? 1 : 0;
+    return VSBP_OK;
+}
+
+int bp_timing_read(vsbp_bp *c, double *ms, int64_t *launches, double *bytes)
+{
+    if (!c || !ms || !launches || !bytes) return VSBP_EINVAL;
+    if (!c->timing) return VSBP_EINVAL;
+    int rc = timing_drain(c);
+    if (rc) return rc;
+    for (int l = 0; l < 16; ++l) {
+        ms[l] = c->acc_ms[l];
+        launches[l] = c->acc_launches[l];
+        bytes[l] = c->acc_bytes[l];
+        c->acc_ms[l] = 0.0;
+        c->acc_launches[l] = 0;
+        c->acc_bytes[l] = 0.0;
+    }
+    return VSBP_OK;
+}
+
+void bp_destroy(vsbp_bp *c)
+{
+    if (c && c->timing) bp_timing_enable(c, 0);
+    delete c;
+}
+
+int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
+                       float sigma_s, float sigma_r, int radius, void *stream)
+{
+    if (B < 1 || !disp_lo || !guide_rgb || !disp_hi || W < 1 || H < 1) return VSBP_EINVAL;
+    if (s < 1 || s > 16 || radius < 1 || radius > 8 || !(sigma_s > 0.f) || !(sigma_r > 0.f)) return VSBP_EINVAL;
+    if ((long long)W * s * H * s > (1ll << 30)) return VSBP_EINVAL;
+    CK(vsbp::launch_jbu(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int jbu_upsample(const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
+                 float sigma_s, float sigma_r, int radius, void *stream)
+{
+    return jbu_upsample_batch(1, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, stream);
+}
+
+int reproject_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+                    unsigned long long *n_valid, void *stream)
+{
+    if (B < 1 || !disp || !Q || !xyz || !n_valid || W < 1 || H < 1) return VSBP_EINVAL;
+    if (!(min_disp > 0.f)) return VSBP_EINVAL;
+    if ((long long)W * H > (1ll << 30)) return VSBP_EINVAL;
+    float Qf[16];
+    for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
+    CK(cudaMemsetAsync(n_valid, 0, sizeof(unsigned long long) * (size_t)B, (cudaStream_t)stream));
+    CK(vsbp::launch_reproject(B, disp, W, H, Qf, min_disp, xyz, n_valid, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int reproject(const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+              unsigned long long *n_valid, void *stream)
+{
+    return reproject_batch(1, disp, W, H, Q, min_disp, xyz, n_valid, stream);
+}
+
+int prep_downsample_batch(int n, const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *gray_lo, void *stream)
+{
+    if (n < 1 || !rgb_hi || !gray_lo || W_hi < 1 || H_hi < 1 || s < 1 || s > 64) return VSBP_EINVAL;
+    if (W_hi % s != 0 || H_hi % s != 0) return VSBP_EDIM;
+    CK(vsbp::launch_prep(n, rgb_hi, W_hi, H_hi, s, gray_lo, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int prep_downsample(const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *gray_lo, void *stream)
+{
+    return prep_downsample_batch(1, rgb_hi, W_hi, H_hi, s, gray_lo, stream);
+}
+
+int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsigned long long *n_valid,
+                       uint64_t first_pair_id, vsbp_summary *summary, void *stream)
+{
+    if (B < 1 || !disp_lo || !summary || W < 1 || H < 1) return VSBP_EINVAL;
+    CK(vsbp::launch_summary(B, disp_lo, W, H, n_valid, first_pair_id, summary, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,118 @@
+// vsbp_internal.cuh -- device-side layout helpers shared by the vsbp kernels.
+//
+// HBM layout of one pyramid level l (W_l x H_l, Wc = ceil(W_l/2)), DESIGN.md §7:
+//   pixels are split by checkerboard colour c = (x+y)&1 (R-10) and stored
+//   compactly per row: pixel (x,y) -> (c, y, i = x>>1).  A colour-c iteration
+//   then reads only colour 1-c messages and writes only colour c ones, both as
+//   contiguous runs along i.
+//   cost  D_l : [B][2][H_l][Wc][Lp]       element type TD_l (u8/u16/i32 per level)
+//   msgs  M_l : [B][2][4][H_l][Wc][Lp]    element type TM (u8/u16/i32)
+//   M_l[b][c][k][y][i][d] = message that pixel (x,y) SENDS toward direction k
+//   (0 up, 1 down, 2 left, 3 right).  Lp = L rounded up to 16; labels >= L are 0.
+// Each thread owns one 16-label chunk of one pixel: a 16-byte vector at u8,
+// 32 bytes at u16, 64 bytes at i32.  The G = pow2 >= Lp/16 threads of one pixel
+// are adjacent lanes of a warp.
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vsbp {
+
+constexpr int CH = 16;                       // labels per thread chunk
+constexpr int BIG = 0x7FF00000;              // > any belief (bp_create bound, R-25)
+constexpr unsigned FULL = 0xffffffffu;
+
+__host__ __device__ __forceinline__ size_t d_off(int b, int c, int y, int i, int H, int Wc, int Lp)
+{
+    return ((((size_t)b * 2 + c) * H + y) * Wc + i) * (size_t)Lp;
+}
+
+__host__ __device__ __forceinline__ size_t m_off(int b, int c, int k, int y, int i, int H, int Wc, int Lp)
+{
+    return (((((size_t)b * 2 + c) * 4 + k) * H + y) * Wc + i) * (size_t)Lp;
+}
+
+// ---------------------------------------------------------------- 16-label chunk I/O
+template <typename T> struct Chunk;
+
+template <> struct Chunk<uint8_t> {
+    static __device__ __forceinline__ void load(const uint8_t *p, int v[CH])
+    {
+        uint4 w = __ldg(reinterpret_cast<const uint4 *>(p));
+        unsigned u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+#pragma unroll
+            for (int b = 0; b < 4; ++b) v[4 * q + b] = (u[q] >> (8 * b)) & 0xff;
+    }
+    static __device__ __forceinline__ void store(uint8_t *p, const int v[CH])
+    {
+        unsigned u[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q)
+            u[q] = (unsigned)v[4 * q] | ((unsigned)v[4 * q + 1] << 8) | ((unsigned)v[4 * q + 2] << 16) |
+                   ((unsigned)v[4 * q + 3] << 24);
+        *reinterpret_cast<uint4 *>(p) = make_uint4(u[0], u[1], u[2], u[3]);
+    }
+};
+
+template <> struct Chunk<uint16_t> {
+    static __device__ __forceinline__ void load(const uint16_t *p, int v[CH])
+    {
+        const uint4 *q4 = reinterpret_cast<const uint4 *>(p);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            uint4 w = __ldg(q4 + h);
+            unsigned u[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                v[8 * h + 2 * q] = u[q] & 0xffff;
+                v[8 * h + 2 * q + 1] = u[q] >> 16;
+            }
+        }
+    }
+    static __device__ __forceinline__ void store(uint16_t *p, const int v[CH])
+    {
+        uint4 *q4 = reinterpret_cast<uint4 *>(p);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            unsigned u[4];
+#pragma unroll
+            for (int q = 0; q < 4; ++q)
+                u[q] = (unsigned)v[8 * h + 2 * q] | ((unsigned)v[8 * h + 2 * q + 1] << 16);
+            q4[h] = make_uint4(u[0], u[1], u[2], u[3]);
+        }
+    }
+};
+
+template <> struct Chunk<int32_t> {
+    static __device__ __forceinline__ void load(const int32_t *p, int v[CH])
+    {
+        const int4 *q4 = reinterpret_cast<const int4 *>(p);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) {
+            int4 w = __ldg(q4 + h);
+            v[4 * h] = w.x;
+            v[4 * h + 1] = w.y;
+            v[4 * h + 2] = w.z;
+            v[4 * h + 3] = w.w;
+        }
+    }
+    static __device__ __forceinline__ void store(int32_t *p, const int v[CH])
+    {
+        int4 *q4 = reinterpret_cast<int4 *>(p);
+#pragma unroll
+        for (int h = 0; h < 4; ++h) q4[h] = make_int4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
+    }
+};
+
+__device__ __forceinline__ void zero16(int v[CH])
+{
+#pragma unroll
+    for (int j = 0; j < CH; ++j) v[j] = 0;
+}
+
+// thread-local launch accounting (host side)
+void note_launch(int n = 1);
+
+}  // namespace vsbp

@@ -1,0 +1,36 @@
+// vsbp_kernels.h -- host-side launchers of the vsbp kernels (internal).
+#pragma once
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace vsbp {
+
+// Geometry of one launch: the level being processed (W,H,Wc) and, where used,
+// its parent level (Wp,Hp,Wcp); label padding and the lane-group width G.
+struct Geom {
+    int B;
+    int W, H, Wc;
+    int Wp, Hp, Wcp;
+    int L, Lp, nch, G, log2G;
+};
+
+cudaError_t launch_costvol(const uint8_t *left, const uint8_t *right, void *D, int dbytes, const Geom &g, int lam_q,
+                           int tau_d, cudaStream_t st);
+cudaError_t launch_pyramid(const void *Dc, int cbytes, void *Dp, int pbytes, const Geom &g, cudaStream_t st);
+cudaError_t launch_update(const void *D, int dbytes, void *M, const void *Mp, int mbytes, const Geom &g, int mode,
+                          int colour, int S, int tau_q, cudaStream_t st);
+cudaError_t launch_upcopy(void *M, const void *Mp, int mbytes, const Geom &g, int colour, cudaStream_t st);
+cudaError_t launch_wta(const void *D, int dbytes, const void *M, int mbytes, const Geom &g, int32_t *disp,
+                       cudaStream_t st);
+cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
+cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
+
+cudaError_t launch_jbu(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
+                       float sigma_s, float sigma_r, int radius, cudaStream_t st);
+cudaError_t launch_reproject(int B, const float *disp, int W, int H, const float Qf[16], float min_disp, float *xyz,
+                             unsigned long long *n_valid, cudaStream_t st);
+cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray, cudaStream_t st);
+cudaError_t launch_summary(int B, const int32_t *disp, int W, int H, const unsigned long long *n_valid,
+                           uint64_t first_pair_id, void *summary, cudaStream_t st);
+
+}  // namespace vsbp

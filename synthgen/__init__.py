@@ -57,28 +57,25 @@ def row_plane_pair(seed: int, W: int, H: int, dmin: int, dmax: int):
 # ----------------------------------------------------------------------------- RGB
 def value_noise_rgb(seed: int, W: int, H: int, cells=(64, 32, 16, 8, 4), iid_amp: int = 8) -> np.ndarray:
     """Multi-octave bilinear value noise (cells in full-res px, amplitudes halving)
-    plus i.i.d. +-iid_amp per channel; u8 [H][W][3]."""
+    plus i.i.d. +-iid_amp per channel; u8 [H][W][3].  Pixel (x, y) samples the
+    lattice at ((x+0.5)/c, (y+0.5)/c); the interpolation is separable."""
     g = rng(seed)
     acc = np.zeros((H, W, 3), np.float32)
     amp, total = 1.0, 0.0
     for c in cells:
         gh, gw = H // c + 2, W // c + 2
         lat = g.random((gh, gw, 3), dtype=np.float32)
-        ys = (np.arange(H, dtype=np.float32) + 0.5) / c
         xs = (np.arange(W, dtype=np.float32) + 0.5) / c
-        y0 = ys.astype(np.int32)
         x0 = xs.astype(np.int32)
-        fy = (ys - y0)[:, None, None]
         fx = (xs - x0)[None, :, None]
-        a = lat[y0][:, x0]
-        b = lat[y0][:, x0 + 1]
-        cc = lat[y0 + 1][:, x0]
-        d = lat[y0 + 1][:, x0 + 1]
-        acc += amp * ((a * (1 - fx) + b * fx) * (1 - fy) + (cc * (1 - fx) + d * fx) * fy)
+        A = lat[:, x0] * (1 - fx) + lat[:, x0 + 1] * fx          # (gh, W, 3)
+        fy = ((np.arange(c, dtype=np.float32) + 0.5) / c)[None, :, None, None]
+        rows = A[:-1, None] * (1 - fy) + A[1:, None] * fy        # (gh-1, c, W, 3)
+        acc += amp * rows.reshape(-1, W, 3)[:H]
         total += amp
         amp *= 0.5
     img = acc * (255.0 / total)
-    img += g.integers(-iid_amp, iid_amp + 1, size=(H, W, 3)).astype(np.float32)
+    img += g.integers(-iid_amp, iid_amp + 1, size=(H, W, 3), dtype=np.int16).astype(np.float32)
     return np.clip(np.rint(img), 0, 255).astype(np.uint8)
 
 

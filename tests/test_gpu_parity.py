@@ -1,0 +1,227 @@
+"""GPU parity (-m gpu): the CUDA path through the C ABI against the CPU oracle on
+the same seeded inputs.  BP (costs, every level's messages, disparities) must be
+bit-exact; JBU within 1e-4 full-res px; XYZ within 1e-5 relative."""
+import numpy as np
+import pytest
+import torch
+
+import oracle
+import synthgen
+
+pytestmark = pytest.mark.gpu
+
+if torch.cuda.is_available():
+    import paper_1902_09733_b200 as P
+
+
+def dev():
+    return torch.device("cuda:0")
+
+
+def to_dev(a):
+    return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
+
+
+def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, batch=None):
+    left = np.asarray(left)
+    right = np.asarray(right)
+    if left.ndim == 2:
+        left, right = left[None], right[None]
+    B, H, W = left.shape
+    bp = P.StereoBP(W, H, L, levels, iters, lam, dt, st, batch=batch or B, msg_bytes=msg_bytes, device=dev())
+    disp = bp.disparity(to_dev(left), to_dev(right))
+    torch.cuda.synchronize()
+    return bp, disp.cpu().numpy()
+
+
+def check_bp_case(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, all_levels=True):
+    bp, disp = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes)
+    d_o, msgs_o = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
+    assert np.array_equal(disp[0], d_o), "disparity differs"
+    levels_to_check = range(levels) if all_levels else [0]
+    q = oracle.quantize(lam, dt, st)
+    D = oracle.cost_volume(left, right, L, q)
+    for l in levels_to_check:
+        m_g = bp.messages(0, l).cpu().numpy()
+        assert np.array_equal(m_g, msgs_o[l]), f"messages differ on level {l}"
+        c_g = bp.costs(0, l).cpu().numpy()
+        assert np.array_equal(c_g, D), f"costs differ on level {l}"
+        if l + 1 < levels:
+            D = oracle.pyramid_down(D)
+    return disp[0]
+
+
+# ----------------------------------------------------------------------------- BP
+def test_config1_shift():
+    l, r = synthgen.shifted_pair(1, 64, 48, 5)
+    disp = check_bp_case(l, r, 16, 1, 5)
+    assert np.mean(disp[:, 5:] == 5) >= 0.999
+
+
+def test_config1_row_plane_hierarchical():
+    l, r, _ = synthgen.row_plane_pair(2, 64, 48, 1, 12)
+    check_bp_case(l, r, 16, 3, 5)
+
+
+@pytest.mark.parametrize("seed", range(40))
+def test_bp_fuzz(seed):
+    rng = np.random.default_rng(1000 + seed)
+    W = int(rng.choice([1, 2, 3, int(rng.integers(4, 71))]))
+    H = int(rng.choice([1, 2, int(rng.integers(3, 71))]))
+    L = int(rng.choice([2, 3, 16, 17, 31, 64, int(rng.integers(2, 131))]))
+    levels = int(rng.integers(1, 7))
+    iters = int(rng.integers(1, 13))
+    lam = float(rng.choice([0.0, 0.07, 0.3, 1.0]))
+    dt = float(rng.choice([1.0, 15.0, 40.0]))
+    st = float(rng.choice([0.01, 1.7, 3.0, 40.0]))
+    left = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    right = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    try:
+        oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st)
+    except oracle.OracleError as e:
+        with pytest.raises(P.VsbpError) as ge:
+            run_gpu_bp(left, right, L, levels, iters, lam, dt, st)
+        assert ge.value.code == e.code
+        return
+    check_bp_case(left, right, L, levels, iters, lam, dt, st)
+
+
+@pytest.mark.parametrize("msg_bytes", [1, 2, 4])
+def test_storage_widths_agree(msg_bytes):
+    l, r, _ = synthgen.row_plane_pair(3, 97, 61, 2, 20)
+    check_bp_case(l, r, 32, 4, 5, msg_bytes=msg_bytes)
+
+
+def test_wide_tau_q_u16_and_i32_storage():
+    rng = np.random.default_rng(5)
+    l = rng.integers(0, 256, size=(33, 45), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(33, 45), dtype=np.uint8)
+    check_bp_case(l, r, 24, 3, 4, lam=2.0, dt=60.0, st=100.0)     # tau_q = 12800 -> u16
+    check_bp_case(l, r, 24, 2, 3, lam=2.0, dt=60.0, st=1000.0)    # tau_q = 128000 -> i32
+
+
+def test_batch_equals_single():
+    pairs = [synthgen.shifted_pair(10 + i, 80, 50, 3 + i) for i in range(3)]
+    left = np.stack([p[0] for p in pairs])
+    right = np.stack([p[1] for p in pairs])
+    bp, disp = run_gpu_bp(left, right, 16, 3, 5)
+    for i in range(3):
+        assert np.array_equal(disp[i], oracle.bp_disparity(left[i], right[i], 16, 3, 5))
+        _, msgs = oracle.bp_disparity(left[i], right[i], 16, 3, 5, return_messages=True)
+        assert np.array_equal(bp.messages(i, 0).cpu().numpy(), msgs[0])
+
+
+def test_batch_smaller_than_workspace_and_determinism():
+    l, r = synthgen.shifted_pair(4, 70, 40, 6)
+    bp = P.StereoBP(70, 40, 16, 2, 5, batch=4, device=dev())
+    a = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+    b = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+    assert np.array_equal(a, b)
+    assert np.array_equal(a, oracle.bp_disparity(l, r, 16, 2, 5))
+
+
+def c2_pair(seed=0):
+    left, right, d_lo = synthgen.stereo_pair_rgb(seed)
+    return left, right, d_lo, oracle.prep(left, 4), oracle.prep(right, 4)
+
+
+def test_config2_full_size_bit_exact():
+    """676x380, L=64, 5 levels x 5 iterations: disparity and every level's messages."""
+    _, _, d_lo, gl, gr = c2_pair(0)
+    disp = check_bp_case(gl, gr, 64, 5, 5)
+    assert np.mean(disp == d_lo) > 0.9
+
+
+def test_config4_full_size_bit_exact():
+    """1352x760, L=128, 6 levels x 8 iterations: disparity and level-0 messages."""
+    left, right, d_lo = synthgen.stereo_pair_rgb(1, s=2, dmin=16, dmax=96)
+    gl, gr = oracle.prep(left, 2), oracle.prep(right, 2)
+    disp = check_bp_case(gl, gr, 128, 6, 8, all_levels=False)
+    assert np.mean(disp == d_lo) > 0.85
+
+
+# ----------------------------------------------------------------------------- a0
+@pytest.mark.parametrize("s", [1, 2, 3, 4, 8])
+def test_prep_bit_exact(s):
+    rgb = synthgen.value_noise_rgb(20 + s, 120, 72)  # 120 x 72 divides by 1, 2, 3, 4, 8
+    g = P.prep_downsample(to_dev(rgb), s).cpu().numpy()
+    assert np.array_equal(g, oracle.prep(rgb, s))
+
+
+def test_prep_full_frame_batch():
+    frames = np.stack([synthgen.value_noise_rgb(30 + i, 2704, 1520) for i in range(2)])
+    g = P.prep_downsample(to_dev(frames), 4).cpu().numpy()
+    for i in range(2):
+        assert np.array_equal(g[i], oracle.prep(frames[i], 4))
+
+
+# ----------------------------------------------------------------------------- a6
+@pytest.mark.parametrize("s,r,ss,sr", [(2, 1, 1.3, 40.0), (3, 2, 2.0, 20.0), (4, 2, 3.75, 15.0), (4, 5, 3.75, 15.0),
+                                       (2, 3, 7.5, 15.0), (1, 4, 2.0, 30.0), (5, 3, 3.0, 8.0)])
+def test_jbu_small(s, r, ss, sr):
+    rng = np.random.default_rng(s * 10 + r)
+    lo = rng.integers(0, 64, size=(13, 19)).astype(np.int32)
+    guide = synthgen.value_noise_rgb(s + r, 19 * s, 13 * s)
+    got = P.jbu_upsample(to_dev(lo), to_dev(guide), s, ss, sr, r).cpu().numpy().astype(np.float64)
+    ref = oracle.jbu(lo, guide, s, ss, sr, r)
+    assert np.max(np.abs(got - ref)) <= 1e-4
+
+
+def test_jbu_adversarial_colours():
+    """Every tap far in colour from the pixel (large |logit|) still within 1e-4."""
+    s, r = 4, 2
+    rng = np.random.default_rng(77)
+    lo = rng.integers(0, 64, size=(10, 12)).astype(np.int32)
+    guide = np.where(rng.random((40, 48, 1)) < 0.5, 0, 255).astype(np.uint8).repeat(3, axis=2)
+    guide = np.ascontiguousarray(guide)
+    got = P.jbu_upsample(to_dev(lo), to_dev(guide), s, 3.75, 15.0, r).cpu().numpy().astype(np.float64)
+    ref = oracle.jbu(lo, guide, s, 3.75, 15.0, r)
+    assert np.max(np.abs(got - ref)) <= 1e-4
+
+
+def test_jbu_full_frame_config3():
+    left, _, d_lo = synthgen.stereo_pair_rgb(2)
+    got = P.jbu_upsample(to_dev(d_lo), to_dev(left), 4, 3.75, 15.0, 2).cpu().numpy().astype(np.float64)
+    ref = oracle.jbu(d_lo, left, 4, 3.75, 15.0, 2)
+    assert np.max(np.abs(got - ref)) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- a7
+def test_reproject_matches_oracle():
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    assert np.array_equal(Q, P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"]))
+    rng = np.random.default_rng(3)
+    disp = rng.uniform(0.0, 256.0, size=(1520, 2704)).astype(np.float32)
+    disp[rng.random(disp.shape) < 0.1] = 0.5  # below min_disp
+    xyz_g, n_g = P.reproject(to_dev(disp), Q, 1.0)
+    xyz_g = xyz_g.cpu().numpy().astype(np.float64)
+    xyz_o, n_o = oracle.reproject(disp.astype(np.float64), Q, 1.0)
+    assert int(n_g.cpu()[0]) == n_o
+    valid = ~np.isnan(xyz_o[..., 0])
+    assert np.array_equal(valid, ~np.isnan(xyz_g[..., 0]))
+    err = np.linalg.norm(xyz_g[valid] - xyz_o[valid], axis=1) / np.linalg.norm(xyz_o[valid], axis=1)
+    assert err.max() <= 1e-5
+
+
+# ----------------------------------------------------------------------------- a0-a8
+def test_pipeline_config3_end_to_end():
+    left, right, _ = synthgen.stereo_pair_rgb(3)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    pipe = P.StereoPipeline(2704, 1520, 4, 64, 5, 5, batch=2, Q=Q, device=dev())
+    lt = to_dev(np.stack([left, left]))
+    rt = to_dev(np.stack([right, right]))
+    summ = pipe.run(lt, rt, first_pair_id=40).cpu().numpy()
+    disp_o, hi_o, xyz_o, n_o = oracle.pipeline_pair(left, right, 4, 64, 5, 5, Q)
+    for b in range(2):
+        assert np.array_equal(pipe.disp[b].cpu().numpy(), disp_o)
+        hi_g = pipe.disp_hi[b].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(hi_g - hi_o)) <= 1e-4
+        ls, lh = oracle.disp_summary(disp_o)
+        assert int(summ[b, 1]) == ls
+        assert int(summ[b, 2]) & 0xFFFFFFFFFFFFFFFF == lh
+        assert int(summ[b, 3]) == 40 + b
+        # count: equal up to pixels whose disparity is within 1e-4 of min_disp
+        amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
+        assert abs(int(summ[b, 0]) - n_o) <= amb
