@@ -218,20 +218,23 @@ __global__ void __launch_bounds__(256) k_upcopy(TM *__restrict__ M, const TM *__
 // ======================================================================== a5
 template <typename TD, typename TM>
 __global__ void __launch_bounds__(256) k_wta(const TD *__restrict__ D, const TM *__restrict__ M, Geom g,
-                                             int32_t *__restrict__ disp)
+                                             int32_t *__restrict__ disp, int only_colour)
 {
+    // only_colour < 0: both colours; else only pixels of that colour
     const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
     const int lane_g = threadIdx.x & (g.G - 1);
     const long pix = gt >> g.log2G;
     const long per_c = (long)g.H * g.Wc;
-    bool active = pix < (long)g.B * 2 * per_c;
+    const int ncol = only_colour < 0 ? 2 : 1;
+    bool active = pix < (long)g.B * ncol * per_c;
     if (__all_sync(FULL, !active)) return;
     int b = 0, c = 0, y = 0, i = 0, x = 0;
     if (active) {
-        b = (int)(pix / (2 * per_c));
-        long r = pix - (long)b * 2 * per_c;
+        b = (int)(pix / (ncol * per_c));
+        long r = pix - (long)b * ncol * per_c;
         c = (int)(r / per_c);
         r -= (long)c * per_c;
+        if (only_colour >= 0) c = only_colour;
         y = (int)(r / g.Wc);
         i = (int)(r - (long)y * g.Wc);
         x = 2 * i + ((c + y) & 1);
@@ -284,7 +287,7 @@ __global__ void k_export_msgs(const TM *__restrict__ M, Geom g, int b, int32_t *
         r /= g.W;
         const int y = (int)(r % g.H);
         const int k = (int)(r / g.H);
-        out[t] = (int32_t)M[m_off(b, (x + y) & 1, k, y, x >> 1, g.H, g.Wc, g.Lp) + d];
+        out[t] = (int32_t)M[m_off(b, (x + y) & 1, k, y, x >> 1, g.H, g.Wc, g.Lp) + pos_of_label<TM>(d)];
     }
 }
 
@@ -297,7 +300,7 @@ __global__ void k_export_costs(const TD *__restrict__ D, Geom g, int b, int32_t 
         long r = t / g.L;
         const int x = (int)(r % g.W);
         const int y = (int)(r / g.W);
-        out[t] = (int32_t)D[d_off(b, (x + y) & 1, y, x >> 1, g.H, g.Wc, g.Lp) + d];
+        out[t] = (int32_t)D[d_off(b, (x + y) & 1, y, x >> 1, g.H, g.Wc, g.Lp) + pos_of_label<TD>(d)];
     }
 }
 
@@ -361,13 +364,13 @@ cudaError_t launch_upcopy(void *M, const void *Mp, int mbytes, const Geom &g, in
 }
 
 cudaError_t launch_wta(const void *D, int dbytes, const void *M, int mbytes, const Geom &g, int32_t *disp,
-                       cudaStream_t st)
+                       int only_colour, cudaStream_t st)
 {
-    const long threads = (long)g.B * 2 * g.H * g.Wc * g.G;
+    const long threads = (long)g.B * (only_colour < 0 ? 2 : 1) * g.H * g.Wc * g.G;
     VSBP_DISPATCH_T(dbytes, TD,
                     VSBP_DISPATCH_T(mbytes, TM,
-                                    k_wta<TD, TM><<<blocks_for(threads), 256, 0, st>>>((const TD *)D,
-                                                                                       (const TM *)M, g, disp)));
+                                    k_wta<TD, TM><<<blocks_for(threads), 256, 0, st>>>(
+                                        (const TD *)D, (const TM *)M, g, disp, only_colour)));
     note_launch();
     return cudaGetLastError();
 }

@@ -154,8 +154,16 @@ __global__ void __launch_bounds__(256) k_reproject(const float *__restrict__ dis
         o[1] = o1;
         o[2] = o2;
     }
+    // one atomic per block: warp ballots -> shared-memory sum
+    __shared__ unsigned warp_cnt[8];
     const unsigned m = __ballot_sync(FULL, valid);
-    if ((threadIdx.x & 31) == 0 && m) atomicAdd(n_valid + b, (unsigned long long)__popc(m));
+    if ((threadIdx.x & 31) == 0) warp_cnt[threadIdx.x >> 5] = __popc(m);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned n = 0;
+        for (int w = 0; w < (int)(blockDim.x >> 5); ++w) n += warp_cnt[w];
+        if (n) atomicAdd(n_valid + b, (unsigned long long)n);
+    }
 }
 
 // ======================================================================== a8

@@ -98,6 +98,17 @@ vsbp::Geom geom(const vsbp_bp *c, int B, int l)
 
 inline char *wsp(const vsbp_bp *c) { return (char *)c->ws; }
 
+// The packed kernel (bp_fast.cu) is exact when messages are u8 (tau_q <= 255 <= 2S,
+// so the 3-tap stencil is the truncated-linear envelope), the level's costs are
+// u8/u16 and every belief fits 16 bits, and L <= 512 (9-bit WTA key).
+bool use_fast(const vsbp_bp *c, int l)
+{
+    if (c->kernel != 0 || c->msg_bytes != 1 || c->S != 128 || c->tau_q > 255 || c->L > 512) return false;
+    if (c->dbytes[l] > 2) return false;
+    const long long dmax = ((long long)c->lam_q * c->tau_d) << (2 * l);
+    return dmax + 4LL * c->tau_q < 65536LL;
+}
+
 }  // namespace
 
 namespace vsbp {
@@ -288,9 +299,15 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         const int slot = (c->timing && c->n_pending < 64) ? c->n_pending++ : -1;
         if (slot >= 0) CK(cudaEventRecord(c->ev[slot][0], st));
         double bytes = 0.0;
+        const bool fast = use_fast(c, l);
         for (int t = 0; t < c->iters; ++t) {
             const int mode = (t > 0) ? 0 : (l == top ? 1 : 2);
-            CK(vsbp::launch_update(D, c->dbytes[l], M, Mp, c->msg_bytes, g, mode, t & 1, c->S, c->tau_q, st));
+            if (fast) {
+                int32_t *wta = (l == 0 && t == c->iters - 1) ? disp : nullptr;  // a5 fused for this colour
+                CK(vsbp::launch_update_fast(D, c->dbytes[l], M, Mp, g, mode, t & 1, c->S, c->tau_q, wta, st));
+            } else {
+                CK(vsbp::launch_update(D, c->dbytes[l], M, Mp, c->msg_bytes, g, mode, t & 1, c->S, c->tau_q, st));
+            }
             // pixels of colour t&1: ceil/floor split of each row
             long long npix = 0;
             for (int y = 0; y < g.H; ++y) npix += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;
@@ -303,10 +320,11 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
             c->ev_bytes[slot] = bytes;
         }
     }
-    // a5
+    // a5 (the colour updated last was labelled inside its update when the fast kernel ran)
     {
         vsbp::Geom g = geom(c, B, 0);
-        CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, st));
+        const int only = use_fast(c, 0) ? (((c->iters - 1) & 1) ^ 1) : -1;
+        CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, only, st));
     }
     c->last_B = B;
     return VSBP_OK;

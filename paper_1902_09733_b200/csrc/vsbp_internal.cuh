@@ -33,6 +33,19 @@ __host__ __device__ __forceinline__ size_t m_off(int b, int c, int k, int y, int
 }
 
 // ---------------------------------------------------------------- 16-label chunk I/O
+// Storage order inside a 16-label chunk (u8 and u16 only; i32 is natural):
+//   u8 : byte 4q+b holds label 2q + (b&1) + 8*(b>>1)   (q = 0..3)
+//   u16: element 2j+h holds label j + 8h                (j = 0..7)
+// so that one PRMT (u8) or nothing (u16) yields the packed u16x2 registers
+// r_j = (label j | label j+8 << 16) the fast kernel computes on.  load()/store()
+// below convert to/from natural label order v[0..15].
+__host__ __device__ __forceinline__ int u8_pos_of_label(int l)
+{
+    const int r = l & 7;
+    return 4 * (r >> 1) + (r & 1) + 2 * (l >> 3);
+}
+__host__ __device__ __forceinline__ int u16_pos_of_label(int l) { return 2 * (l & 7) + (l >> 3); }
+
 template <typename T> struct Chunk;
 
 template <> struct Chunk<uint8_t> {
@@ -41,17 +54,20 @@ template <> struct Chunk<uint8_t> {
         uint4 w = __ldg(reinterpret_cast<const uint4 *>(p));
         unsigned u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
-        for (int q = 0; q < 4; ++q)
-#pragma unroll
-            for (int b = 0; b < 4; ++b) v[4 * q + b] = (u[q] >> (8 * b)) & 0xff;
+        for (int q = 0; q < 4; ++q) {
+            v[2 * q] = u[q] & 0xff;
+            v[2 * q + 1] = (u[q] >> 8) & 0xff;
+            v[2 * q + 8] = (u[q] >> 16) & 0xff;
+            v[2 * q + 9] = u[q] >> 24;
+        }
     }
     static __device__ __forceinline__ void store(uint8_t *p, const int v[CH])
     {
         unsigned u[4];
 #pragma unroll
         for (int q = 0; q < 4; ++q)
-            u[q] = (unsigned)v[4 * q] | ((unsigned)v[4 * q + 1] << 8) | ((unsigned)v[4 * q + 2] << 16) |
-                   ((unsigned)v[4 * q + 3] << 24);
+            u[q] = (unsigned)v[2 * q] | ((unsigned)v[2 * q + 1] << 8) | ((unsigned)v[2 * q + 8] << 16) |
+                   ((unsigned)v[2 * q + 9] << 24);
         *reinterpret_cast<uint4 *>(p) = make_uint4(u[0], u[1], u[2], u[3]);
     }
 };
@@ -66,8 +82,8 @@ template <> struct Chunk<uint16_t> {
             unsigned u[4] = {w.x, w.y, w.z, w.w};
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                v[8 * h + 2 * q] = u[q] & 0xffff;
-                v[8 * h + 2 * q + 1] = u[q] >> 16;
+                v[4 * h + q] = u[q] & 0xffff;
+                v[4 * h + q + 8] = u[q] >> 16;
             }
         }
     }
@@ -78,8 +94,7 @@ template <> struct Chunk<uint16_t> {
         for (int h = 0; h < 2; ++h) {
             unsigned u[4];
 #pragma unroll
-            for (int q = 0; q < 4; ++q)
-                u[q] = (unsigned)v[8 * h + 2 * q] | ((unsigned)v[8 * h + 2 * q + 1] << 16);
+            for (int q = 0; q < 4; ++q) u[q] = (unsigned)v[4 * h + q] | ((unsigned)v[4 * h + q + 8] << 16);
             q4[h] = make_uint4(u[0], u[1], u[2], u[3]);
         }
     }
@@ -105,6 +120,14 @@ template <> struct Chunk<int32_t> {
         for (int h = 0; h < 4; ++h) q4[h] = make_int4(v[4 * h], v[4 * h + 1], v[4 * h + 2], v[4 * h + 3]);
     }
 };
+
+// storage index of label d (any chunk) for element type T
+template <typename T> __device__ __forceinline__ int pos_of_label(int d)
+{
+    if (sizeof(T) == 1) return (d & ~15) + u8_pos_of_label(d & 15);
+    if (sizeof(T) == 2) return (d & ~15) + u16_pos_of_label(d & 15);
+    return d;
+}
 
 __device__ __forceinline__ void zero16(int v[CH])
 {

@@ -21,7 +21,9 @@ cudaError_t launch_update(const void *D, int dbytes, void *M, const void *Mp, in
                           int colour, int S, int tau_q, cudaStream_t st);
 cudaError_t launch_upcopy(void *M, const void *Mp, int mbytes, const Geom &g, int colour, cudaStream_t st);
 cudaError_t launch_wta(const void *D, int dbytes, const void *M, int mbytes, const Geom &g, int32_t *disp,
-                       cudaStream_t st);
+                       int only_colour, cudaStream_t st);
+cudaError_t launch_update_fast(const void *D, int dbytes, void *M, const void *Mp, const Geom &g, int mode, int colour,
+                               int S, int tau_q, int32_t *disp_wta, cudaStream_t st);
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 
