@@ -115,7 +115,9 @@ void bp_destroy(vsbp_bp *ctx);
  *   disp_lo   : int32 [B][H][W] low-res labels
  *   guide_rgb : u8 [B][s*H][s*W][3] full-res colour guide (the left frame, R-17)
  *   disp_hi   : float [B][s*H][s*W] upsampled disparity in FULL-RES pixels (x s)
- *   sigma_s   : spatial sigma in LOW-RES pixels (> 0); sigma_r: range sigma on
+ *   sigma_s   : spatial sigma in LOW-RES pixels, with
+ *               log2(e)*(radius+0.5)^2/sigma_s^2 <= 100 (else VSBP_EINVAL: the
+ *               window's weights would leave f32 range); sigma_r: range sigma on
  *               the 0..255 scale (> 0); radius: window half-width in low-res
  *               pixels, 1..8; s: integer scale 1..16.
  * f32 arithmetic; agrees with the double oracle within 1e-4 full-res px.
@@ -125,6 +127,16 @@ int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_
                        float *disp_hi, float sigma_s, float sigma_r, int radius, void *stream);
 int jbu_upsample(const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
                  float sigma_s, float sigma_r, int radius, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * jbu_reproject_batch -- a6 + a7 fused (the pipeline's call): jbu_upsample_batch
+ * followed by reproject_batch on its output, in one kernel, without re-reading
+ * disp_hi.  Arguments as in those two calls; xyz : float [B][s*H][s*W][3];
+ * n_valid : device uint64 [B], overwritten.  Errors: the union of both calls'.
+ * ------------------------------------------------------------------------- */
+int jbu_reproject_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s,
+                        float sigma_s, float sigma_r, int radius, const double *Q, float min_disp,
+                        float *disp_hi, float *xyz, unsigned long long *n_valid, void *stream);
 
 /* ---------------------------------------------------------------------------
  * reproject_batch -- a7, Eq.3 (R-20, R-21):

@@ -11,6 +11,7 @@ Entry points mirror the C ABI (names follow the paper's steps):
       .messages(pair, level) / .costs(pair, level)                   -- parity exports
   jbu_upsample(disp_lo, guide_rgb, s, sigma_s, sigma_r, radius)      -- a6 (Eq.2)
   reproject(disp, Q, min_disp)                                       -- a7 (Eq.3)
+  jbu_reproject(disp_lo, guide_rgb, s, ..., Q, min_disp)             -- a6 + a7 fused
   prep_downsample(rgb, s)                                            -- a0
   pair_summary(disp_lo, n_valid, first_pair_id)                      -- a8
   StereoPipeline                                                     -- a0-a8 for a batch of pairs
@@ -56,6 +57,9 @@ _EXPORTS = {
                                      C.c_float, C.c_float, C.c_int, C.c_void_p]),
     "jbu_upsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_float,
                                C.c_float, C.c_int, C.c_void_p]),
+    "jbu_reproject_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_float,
+                                      C.c_float, C.c_int, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
+                                      C.c_void_p, C.c_void_p]),
     "reproject_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p,
                                   C.c_void_p, C.c_void_p]),
     "reproject": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p,
@@ -250,6 +254,31 @@ def reproject(disp: torch.Tensor, Q, min_disp: float = 1.0, xyz: torch.Tensor | 
     return xyz, n_valid
 
 
+def jbu_reproject(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_s: float, sigma_r: float,
+                  radius: int, Q, min_disp: float = 1.0, disp_hi: torch.Tensor | None = None,
+                  xyz: torch.Tensor | None = None, n_valid: torch.Tensor | None = None, stream=None):
+    """a6 + a7 fused: -> (disp_hi float32 [B,sH,sW], xyz float32 [B,sH,sW,3], n_valid int64 [B])."""
+    if disp_lo.dim() == 2:
+        disp_lo, guide_rgb = disp_lo.unsqueeze(0), guide_rgb.unsqueeze(0)
+    B, H, W = disp_lo.shape
+    if tuple(guide_rgb.shape) != (B, H * s, W * s, 3):
+        raise ValueError("guide must be [B, s*H, s*W, 3]")
+    dev = disp_lo.device
+    if disp_hi is None:
+        disp_hi = torch.empty((B, H * s, W * s), dtype=torch.float32, device=dev)
+    if xyz is None:
+        xyz = torch.empty((B, H * s, W * s, 3), dtype=torch.float32, device=dev)
+    if n_valid is None:
+        n_valid = torch.empty(B, dtype=torch.int64, device=dev)
+    Qh = np.ascontiguousarray(np.asarray(Q, np.float64).reshape(16))
+    _check(lib().jbu_reproject_batch(B, _dev(disp_lo, torch.int32, "disp_lo"), W, H,
+                                     _dev(guide_rgb, torch.uint8, "guide_rgb"), s, sigma_s, sigma_r, radius,
+                                     Qh.ctypes.data_as(C.c_void_p), min_disp, _dev(disp_hi, torch.float32, "disp_hi"),
+                                     _dev(xyz, torch.float32, "xyz"), _dev(n_valid, torch.int64, "n_valid"),
+                                     _stream(stream)), "jbu_reproject_batch")
+    return disp_hi, xyz, n_valid
+
+
 SUMMARY_BYTES = 64
 
 
@@ -299,8 +328,7 @@ class StereoPipeline:
         prep_downsample(left_rgb, self.s, out=self.gray[0, :B], stream=stream)
         prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
         self.bp.disparity(self.gray[0, :B], self.gray[1, :B], out=self.disp[:B], stream=stream)
-        jbu_upsample(self.disp[:B], left_rgb, self.s, self.sigma_s, self.sigma_r, self.radius,
-                     out=self.disp_hi[:B], stream=stream)
-        reproject(self.disp_hi[:B], self.Q, self.min_disp, xyz=self.xyz[:B], n_valid=self.n_valid[:B],
-                  stream=stream)
+        jbu_reproject(self.disp[:B], left_rgb, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
+                      self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
+                      stream=stream)
         return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=self.summary[:B], stream=stream)

@@ -1,7 +1,6 @@
-// pipeline_kernels.cu -- rows a0, a6, a7, a8 of the hot path on sm_100a.
+// pipeline_kernels.cu -- rows a0, a7, a8 of the hot path on sm_100a (a6: jbu_fast.cu).
 //
 //   k_prep       a0  RGB -> grey (77R+150G+29B+128)>>8 -> s x s mean, half up  P:26, R-22
-//   k_jbu        a6  joint bilateral upsampling, Eq.2, f32                      P:34-38, R-15..R-19, R-24
 //   k_reproject  a7  [X Y Z W]^T = Q [u v d 1]^T, NaN below min_disp          P:40-44 Eq.3, R-20, R-21
 //   k_summary    a8  label sum + order-independent label hash per pair
 #include <math.h>
@@ -32,93 +31,6 @@ __global__ void __launch_bounds__(256) k_prep(const uint8_t *__restrict__ rgb, i
     }
     const int n2 = s * s;
     gray[t] = (uint8_t)((sum + n2 / 2) / n2);
-}
-
-// ======================================================================== a6
-// Block = 32 x 8 full-res pixels of one pair.  The low-res taps it can touch
-// (window centres floor(x/s) +- r) are staged once in shared memory: the guide
-// sample I_q packed as u8x4 and the label D'_q.
-constexpr int JBU_BX = 32, JBU_BY = 8, JBU_RMAX = 8;
-constexpr int JBU_LW = JBU_BX + 2 * JBU_RMAX, JBU_LH = JBU_BY + 2 * JBU_RMAX;
-
-struct JbuArgs {
-    int W, H, s, r;
-    float inv_s;
-    float cs;  // log2(e) / (2 sigma_s^2), sigma_s in low-res px
-    float cr;  // log2(e) / (2 sigma_r^2)
-};
-
-__global__ void __launch_bounds__(256) k_jbu(const int32_t *__restrict__ disp_lo, const uint8_t *__restrict__ guide,
-                                             float *__restrict__ disp_hi, JbuArgs a)
-{
-    __shared__ unsigned sI[JBU_LW * JBU_LH];
-    __shared__ int sD[JBU_LW * JBU_LH];
-    const int b = blockIdx.z;
-    const int Wh = a.W * a.s, Hh = a.H * a.s;
-    const int x0 = blockIdx.x * JBU_BX, y0 = blockIdx.y * JBU_BY;
-    const int lx0 = x0 / a.s - a.r, ly0 = y0 / a.s - a.r;
-    const int lw = min(x0 + JBU_BX - 1, Wh - 1) / a.s + a.r - lx0 + 1;
-    const int lh = min(y0 + JBU_BY - 1, Hh - 1) / a.s + a.r - ly0 + 1;
-    const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
-    const int32_t *Dl = disp_lo + (size_t)b * a.H * a.W;
-    const int tid = threadIdx.y * JBU_BX + threadIdx.x;
-    for (int e = tid; e < lw * lh; e += JBU_BX * JBU_BY) {
-        const int qy = ly0 + e / lw, qx = lx0 + e % lw;
-        unsigned I = 0;
-        int dv = -1;  // -1: outside the low-res image, skipped
-        if (qx >= 0 && qy >= 0 && qx < a.W && qy < a.H) {
-            const uint8_t *g = G + ((size_t)(a.s * qy + a.s / 2) * Wh + (size_t)(a.s * qx + a.s / 2)) * 3;
-            I = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
-            dv = Dl[(size_t)qy * a.W + qx];
-        }
-        sI[e] = I;
-        sD[e] = dv;
-    }
-    __syncthreads();
-    const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
-    if (x >= Wh || y >= Hh) return;
-    const uint8_t *gp = G + ((size_t)y * Wh + x) * 3;
-    const unsigned Ip = (unsigned)gp[0] | ((unsigned)gp[1] << 8) | ((unsigned)gp[2] << 16);
-    const float px = (x + 0.5f) * a.inv_s - 0.5f, py = (y + 0.5f) * a.inv_s - 0.5f;
-    const int cx = x / a.s, cy = y / a.s;
-    const int e0 = (cy - a.r - ly0) * lw + (cx - a.r - lx0);
-    const int n = 2 * a.r + 1;
-    // pass 1: the smallest squared colour distance (exact integer)
-    int dmin = 0x7fffffff;
-    for (int ty = 0; ty < n; ++ty)
-        for (int tx = 0; tx < n; ++tx) {
-            const int e = e0 + ty * lw + tx;
-            if (sD[e] < 0) continue;
-            const unsigned ad = __vabsdiffu4(Ip, sI[e]);
-            dmin = min(dmin, (int)__dp4a(ad, ad, 0u));
-        }
-    // pass 2: the largest logit, logit = -cs |p_down - q|^2 - cr (dist2 - dmin)  (log2 units)
-    float lmax = -INFINITY;
-    for (int ty = 0; ty < n; ++ty)
-        for (int tx = 0; tx < n; ++tx) {
-            const int e = e0 + ty * lw + tx;
-            if (sD[e] < 0) continue;
-            const unsigned ad = __vabsdiffu4(Ip, sI[e]);
-            const float sx = px - (float)(cx - a.r + tx), sy = py - (float)(cy - a.r + ty);
-            const float l = -a.cs * (sx * sx + sy * sy) - a.cr * (float)((int)__dp4a(ad, ad, 0u) - dmin);
-            lmax = fmaxf(lmax, l);
-        }
-    // pass 3: Eq.2 with w = 2^(logit - max), accumulated relative to the centre label
-    const int dc = sD[e0 + a.r * lw + a.r];
-    float num = 0.f, den = 0.f;
-    for (int ty = 0; ty < n; ++ty)
-        for (int tx = 0; tx < n; ++tx) {
-            const int e = e0 + ty * lw + tx;
-            const int dq = sD[e];
-            if (dq < 0) continue;
-            const unsigned ad = __vabsdiffu4(Ip, sI[e]);
-            const float sx = px - (float)(cx - a.r + tx), sy = py - (float)(cy - a.r + ty);
-            const float l = -a.cs * (sx * sx + sy * sy) - a.cr * (float)((int)__dp4a(ad, ad, 0u) - dmin);
-            const float w = exp2f(l - lmax);
-            num = fmaf(w, (float)(dq - dc), num);
-            den += w;
-        }
-    disp_hi[((size_t)b * Hh + y) * Wh + x] = (float)a.s * ((float)dc + num / den);
 }
 
 // ======================================================================== a7
@@ -219,24 +131,6 @@ cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, ui
 {
     const long threads = (long)n * (W_hi / s) * (H_hi / s);
     k_prep<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(rgb, W_hi, H_hi, s, n, gray);
-    note_launch();
-    return cudaGetLastError();
-}
-
-cudaError_t launch_jbu(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
-                       float sigma_s, float sigma_r, int radius, cudaStream_t st)
-{
-    const double log2e = 1.4426950408889634;
-    JbuArgs a;
-    a.W = W;
-    a.H = H;
-    a.s = s;
-    a.r = radius;
-    a.inv_s = (float)(1.0 / s);
-    a.cs = (float)(log2e / (2.0 * (double)sigma_s * sigma_s));
-    a.cr = (float)(log2e / (2.0 * (double)sigma_r * sigma_r));
-    dim3 grid((W * s + JBU_BX - 1) / JBU_BX, (H * s + JBU_BY - 1) / JBU_BY, B);
-    k_jbu<<<grid, dim3(JBU_BX, JBU_BY), 0, st>>>(disp_lo, guide, disp_hi, a);
     note_launch();
     return cudaGetLastError();
 }

@@ -394,13 +394,39 @@ void bp_destroy(vsbp_bp *c)
     delete c;
 }
 
-int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
-                       float sigma_s, float sigma_r, int radius, void *stream)
+static int jbu_check(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, void *disp_hi,
+                     float sigma_s, float sigma_r, int radius)
 {
     if (B < 1 || !disp_lo || !guide_rgb || !disp_hi || W < 1 || H < 1) return VSBP_EINVAL;
     if (s < 1 || s > 16 || radius < 1 || radius > 8 || !(sigma_s > 0.f) || !(sigma_r > 0.f)) return VSBP_EINVAL;
     if ((long long)W * s * H * s > (1ll << 30)) return VSBP_EINVAL;
-    CK(vsbp::launch_jbu(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, (cudaStream_t)stream));
+    const double r5 = radius + 0.5;
+    if (1.4426950408889634 * r5 * r5 / ((double)sigma_s * sigma_s) > 100.0) return VSBP_EINVAL;
+    return VSBP_OK;
+}
+
+int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float *disp_hi,
+                       float sigma_s, float sigma_r, int radius, void *stream)
+{
+    int rc = jbu_check(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius);
+    if (rc) return rc;
+    CK(vsbp::launch_jbu_fast(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, nullptr, 1.0f,
+                             nullptr, nullptr, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int jbu_reproject_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float sigma_s,
+                        float sigma_r, int radius, const double *Q, float min_disp, float *disp_hi, float *xyz,
+                        unsigned long long *n_valid, void *stream)
+{
+    int rc = jbu_check(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius);
+    if (rc) return rc;
+    if (!Q || !xyz || !n_valid || !(min_disp > 0.f)) return VSBP_EINVAL;
+    float Qf[16];
+    for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
+    CK(cudaMemsetAsync(n_valid, 0, sizeof(unsigned long long) * (size_t)B, (cudaStream_t)stream));
+    CK(vsbp::launch_jbu_fast(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, Qf, min_disp, xyz,
+                             n_valid, (cudaStream_t)stream));
     return VSBP_OK;
 }
 

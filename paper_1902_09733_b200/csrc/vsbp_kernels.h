@@ -27,8 +27,9 @@ cudaError_t launch_update_fast(const void *D, int dbytes, void *M, const void *M
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 
-cudaError_t launch_jbu(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
-                       float sigma_s, float sigma_r, int radius, cudaStream_t st);
+cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
+                            float sigma_s, float sigma_r, int radius, const float *Qf, float min_disp, float *xyz,
+                            unsigned long long *n_valid, cudaStream_t st);
 cudaError_t launch_reproject(int B, const float *disp, int W, int H, const float Qf[16], float min_disp, float *xyz,
                              unsigned long long *n_valid, cudaStream_t st);
 cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray, cudaStream_t st);

@@ -106,6 +106,9 @@ def test_other_entry_points_validate():
     assert L.jbu_upsample_batch(1, C.c_void_p(256), 4, 4, C.c_void_p(256), 4, C.c_void_p(256), 0.0, 15.0, 2,
                                 None) == -1
     assert L.prep_downsample_batch(1, C.c_void_p(256), 10, 10, 3, C.c_void_p(256), None) == -2
+    # sigma_s so small that the window's weights leave f32 range is refused
+    assert L.jbu_upsample_batch(1, C.c_void_p(256), 4, 4, C.c_void_p(256), 4, C.c_void_p(256), 0.2, 15.0, 2,
+                                None) == -1
     assert L.vsbp_strerror(-3) == b"int32 fixed-point bound exceeded"
 
 

@@ -225,3 +225,44 @@ def test_pipeline_config3_end_to_end():
         # count: equal up to pixels whose disparity is within 1e-4 of min_disp
         amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
         assert abs(int(summ[b, 0]) - n_o) <= amb
+
+
+def test_jbu_reproject_fused():
+    """a6 + a7 in one kernel: disp_hi within 1e-4 px of the oracle's JBU; xyz within
+    1e-5 relative of the oracle's reprojection of the SAME disp_hi; counts equal."""
+    left, _, d_lo = synthgen.stereo_pair_rgb(4)
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    d_lo = d_lo.copy()
+    d_lo[:40, :50] = 0  # some invalid (d < min_disp) points
+    hi, xyz, n = P.jbu_reproject(to_dev(d_lo), to_dev(left), 4, 3.75, 15.0, 2, Q, 1.0)
+    hi = hi[0].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(hi - oracle.jbu(d_lo, left, 4, 3.75, 15.0, 2))) <= 1e-4
+    xyz_o, n_o = oracle.reproject(hi, Q, 1.0)
+    xyz_g = xyz[0].cpu().numpy().astype(np.float64)
+    assert int(n.cpu()[0]) == n_o
+    valid = ~np.isnan(xyz_o[..., 0])
+    assert np.array_equal(valid, ~np.isnan(xyz_g[..., 0]))
+    err = np.linalg.norm(xyz_g[valid] - xyz_o[valid], axis=1) / np.linalg.norm(xyz_o[valid], axis=1)
+    assert err.max() <= 1e-5
+
+
+@pytest.mark.parametrize("W,H,s,r", [(7, 5, 3, 2), (33, 9, 2, 3), (1, 1, 4, 2), (20, 3, 1, 8), (9, 9, 16, 1)])
+def test_jbu_reproject_ragged(W, H, s, r):
+    rng = np.random.default_rng(W * H + s)
+    # f32 bound (DESIGN.md §7 a6): |err| <= s * 2^-21 * (label spread in a window);
+    # keep s * spread <= 256 so 1e-4 px holds (the configurations have s <= 4)
+    lo = rng.integers(0, min(40, 256 // s), size=(H, W)).astype(np.int32)
+    guide = rng.integers(0, 256, size=(H * s, W * s, 3), dtype=np.uint8)
+    Q = oracle.q_matrix(900.0, 880.0, W * s / 2, H * s / 2, 0.5)
+    hi, xyz, n = P.jbu_reproject(to_dev(lo), to_dev(guide), s, 2.5, 20.0, r, Q, 1.0)
+    hi = hi[0].cpu().numpy().astype(np.float64)
+    assert np.max(np.abs(hi - oracle.jbu(lo, guide, s, 2.5, 20.0, r))) <= 1e-4
+    xyz_o, n_o = oracle.reproject(hi, Q, 1.0)
+    assert int(n.cpu()[0]) == n_o
+    xyz_g = xyz[0].cpu().numpy().astype(np.float64)
+    valid = ~np.isnan(xyz_o[..., 0])
+    assert np.array_equal(valid, ~np.isnan(xyz_g[..., 0]))
+    if valid.any():
+        err = np.linalg.norm(xyz_g[valid] - xyz_o[valid], axis=1) / np.linalg.norm(xyz_o[valid], axis=1)
+        assert err.max() <= 1e-5
