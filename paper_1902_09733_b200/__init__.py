@@ -332,3 +332,51 @@ class StereoPipeline:
                       self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
                       stream=stream)
         return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=self.summary[:B], stream=stream)
+
+
+class StereoStream:
+    """End-to-end driver for a stream of host-resident pairs (the user-facing call):
+    pinned host RGB pairs in, per-pair summaries (and the device-resident disparity /
+    cloud of the last batch) out.  Two device input slots: the host->device copy of
+    batch i+1 runs on a copy stream while batch i computes; each batch's summary is
+    copied back to pinned host memory.  Pure stream plumbing; every step of the path
+    runs in the library's kernels (StereoPipeline)."""
+
+    def __init__(self, pipeline: StereoPipeline, device="cuda"):
+        self.pipe = pipeline
+        dev = torch.device(device)
+        B, Hh, Wh = pipeline.B, pipeline.H_hi, pipeline.W_hi
+        self.slots = [(torch.empty((B, Hh, Wh, 3), dtype=torch.uint8, device=dev),
+                       torch.empty((B, Hh, Wh, 3), dtype=torch.uint8, device=dev)) for _ in range(2)]
+        self.copy_stream = torch.cuda.Stream(device=dev)
+        self.copied = [torch.cuda.Event() for _ in range(2)]
+        self.freed = [torch.cuda.Event() for _ in range(2)]
+        self.summary_host = torch.empty((B, 8), dtype=torch.int64).pin_memory()
+        self.device = dev
+
+    def run(self, batches, first_pair_id: int = 0, gather=None, on_summary=None):
+        """batches: iterable of (left_host, right_host) pinned uint8 [B,H,W,3].
+        Enqueues everything; returns the number of batches.  gather(summary) is
+        called on the compute stream after every batch (e.g. the NCCL all_gather of
+        the summaries); on_summary(i, host tensor) after a final synchronise."""
+        compute = torch.cuda.current_stream(self.device)
+        n = 0
+        for i, (lh, rh) in enumerate(batches):
+            k = i & 1
+            ld, rd = self.slots[k]
+            with torch.cuda.stream(self.copy_stream):
+                self.copy_stream.wait_stream(compute) if i < 2 else self.copy_stream.wait_event(self.freed[k])
+                ld.copy_(lh, non_blocking=True)
+                rd.copy_(rh, non_blocking=True)
+                self.copied[k].record(self.copy_stream)
+            compute.wait_event(self.copied[k])
+            summ = self.pipe.run(ld, rd, first_pair_id=first_pair_id + i * self.pipe.B)
+            self.freed[k].record(compute)
+            if gather is not None:
+                gather(summ)
+            self.summary_host.copy_(summ, non_blocking=True)
+            n += 1
+        if on_summary is not None:
+            compute.synchronize()
+            on_summary(n - 1, self.summary_host)
+        return n

@@ -1,25 +1,31 @@
 // bp_fast.cu -- the packed message-update kernel (row a4, the hot loop), sm_100a.
 //
 // Same operation as k_update (bp_kernels.cu): one checkerboard colour of min-sum
-// messages (Eq.1; R-9..R-12), bit-exact, but specialised for the common
-// parameter domain (checked on the host, vsbp_api.cu):
+// messages (Eq.1; R-9..R-12), bit-exact, specialised for the common
+// parameter domain (checked on the host, vsbp_api.cu use_fast()):
 //   * u8 message storage (tau_q <= 255) and S = 128, so tau_q <= 2S and the
 //     truncated-linear lower envelope is an exact 3-tap stencil:
 //       m(d) = min(h'(d), h'(d-1) + S, h'(d+1) + S),  h' = min(h - min h, tau_q)
 //     (terms |d-d'| >= 2 cost >= 2S >= tau_q; clamping h' at tau_q does not change
 //     min(., tau_q), and every stencil term is <= h'(d) <= tau_q);
-//   * every belief of the level fits 16 bits (D_max + 4*tau_q < 2^16), so two
-//     labels travel in one 32-bit register as u16x2 and the arithmetic runs on
-//     the DPX 16x2 integer datapath (VIMNMX/VIMNMX3/VIADDMNMX .U16x2, plain IADD
-//     on non-negative packed halves, PRMT for the u8 <-> u16x2 conversion).
+//   * every belief of the level fits 16 bits (D_max + 4*255 < 2^16), so two labels
+//     travel in one 32-bit register as u16x2 on the DPX 16x2 integer datapath
+//     (VIMNMX / VIMNMX3 / VIADDMNMX .16x2; plain IADD3 on non-negative halves;
+//     PRMT for u8 <-> u16x2).  When beliefs also fit 15 bits (SIGNED) the
+//     normalise-and-clamp is one signed VIADDMNMX: min(h + (-min h), tau_q).
 // Register j of a thread's 16-label chunk holds (label d0+j, label d0+j+8); the
 // storage order of vsbp_internal.cuh makes that a single PRMT per register.
-// Neighbouring labels across chunks come from the adjacent lanes (2 shuffles per
-// pair of directions); min_d h reduces over the G lanes (log2 G shuffles, two
-// directions per shuffle).  HBM traffic per updated pixel: L*w_D + 8L bytes.
+// Labels across chunks come from the adjacent lanes (2 shuffles per pair of
+// directions); min_d h reduces over the G lanes (two directions per shuffle).
+// Addressing: one 64-bit base per pair, then 32-bit offsets; in the colour-split
+// layout the four incoming messages sit at constant offsets from the pixel's own
+// row offset.  Slots toward missing neighbours are never read (R-11), so they
+// are not zeroed here; the parent read of the first iteration masks them (R-12).
 //
-// WTA (a5) is fused into the last iteration of level 0 for the colour being
-// updated there (its belief D + sum of 4 incoming is already in registers).
+// WTA (a5) is fused into the last iteration of level 0 for the colour updated
+// there (its belief D + sum of 4 incoming is in registers); MODE 3 computes only
+// the WTA (no messages) for the other colour.  HBM traffic per updated pixel:
+// L*w_D + 8L bytes (MODE 3: L*w_D + 4L).
 #include "vsbp_internal.cuh"
 #include "vsbp_kernels.h"
 
@@ -31,6 +37,8 @@ __device__ __forceinline__ uint32_t prmt(uint32_t a, uint32_t b, uint32_t sel)
     asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
     return r;
 }
+
+__device__ __forceinline__ uint32_t iadd3(uint32_t a, uint32_t b, uint32_t c) { return a + b + c; }
 
 // 16 u8 labels in storage order -> r[j] = (label j | label j+8 << 16)
 __device__ __forceinline__ void unpack_u8(const uint4 w, uint32_t r[8])
@@ -68,167 +76,190 @@ template <> struct DLoad<uint16_t> {
     }
 };
 
-// MODE 0: normal iteration; 1: top level t=0 (all incoming 0); 2: lower level t=0
-// (incoming read from the parent level).  PAD: some labels of the chunk are >= L.
-// WTA: also write the WTA label of the updated pixels to disp.
-template <typename TD, int MODE, bool PAD, bool WTA>
-__global__ void __launch_bounds__(256) k_update_fast(const TD *__restrict__ D, uint8_t *__restrict__ M,
-                                                     const uint8_t *__restrict__ Mp, Geom g, int colour,
-                                                     uint32_t SS, uint32_t TT, int32_t *__restrict__ disp)
+// min over the 16 labels of a chunk (both halves), replicated in both halves
+__device__ __forceinline__ uint32_t chunk_min(const uint32_t h[8])
 {
-    const long gt = (long)blockIdx.x * blockDim.x + threadIdx.x;
-    const int lane_g = threadIdx.x & (g.G - 1);
-    const long pix = gt >> g.log2G;
-    const long per_c = (long)g.H * g.Wc;
-    bool active = pix < (long)g.B * per_c;
-    if (__all_sync(FULL, !active)) return;
-    int b = 0, y = 0, i = 0, x = 0;
-    if (active) {
-        b = (int)(pix / per_c);
-        const long r = pix - (long)b * per_c;
-        y = (int)(r / g.Wc);
-        i = (int)(r - (long)y * g.Wc);
-        x = 2 * i + ((colour + y) & 1);
-        active = x < g.W;
-    }
-    const bool io = active && lane_g < g.nch;
-    const int d0 = lane_g * CH;
-    const bool has[4] = {y > 0, y < g.H - 1, x > 0, x < g.W - 1};
+    const uint32_t a = __vimin3_u16x2(h[0], h[1], h[2]);
+    const uint32_t c = __vimin3_u16x2(h[3], h[4], h[5]);
+    const uint32_t d = __vimin3_u16x2(a, c, __vminu2(h[6], h[7]));
+    return __vminu2(d, prmt(d, 0u, 0x1032));
+}
 
-    // ---- loads: the 4 incoming messages (neighbour q sends toward p on slot k^1), D
+// MODE 0: normal iteration; 1: top level t=0 (all incoming 0); 2: lower level t=0
+// (incoming read from the parent level); 3: WTA only (no message update).
+// PAD: some labels of the chunk are >= L.  WTA: write the WTA label of the pixel.
+// SIGNED: beliefs < 2^15, normalise+clamp in one signed VIADDMNMX.
+template <typename TD, int MODE, bool PAD, bool WTA, bool SIGNED>
+__global__ void __launch_bounds__(256) k_update_fast(FastArgs a, const TD *__restrict__ D)
+{
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.y;
+    const int lane_g = threadIdx.x & (a.G - 1);
+    const uint32_t pix = t >> a.log2G;
+    bool active = pix < a.npix;
+    if (__all_sync(FULL, !active)) return;
+    const uint32_t y = a.magic ? __umulhi(pix, a.magic) : pix / (uint32_t)a.Wc;
+    const uint32_t i = pix - y * (uint32_t)a.Wc;
+    const uint32_t o = (a.colour + y) & 1u;
+    const int x = 2 * (int)i + (int)o;
+    active = active && x < a.W;
+    const bool io = active && lane_g < a.nch;
+    const int d0 = lane_g * CH;
+    const bool has[4] = {y > 0, (int)y < a.H - 1, x > 0, x < a.W - 1};
+
+    const uint32_t P = a.plane;                          // H * Wc * Lp
+    const uint32_t r = (y * (uint32_t)a.Wc + i) * (uint32_t)a.Lp + (uint32_t)d0;
+    const uint32_t rowstep = (uint32_t)a.Wc * (uint32_t)a.Lp;
+    uint8_t *Mb = a.M + (size_t)b * a.pairM;
+
+    // ---- loads: incoming messages (neighbour in direction k sends on slot k^1)
     uint4 wi[4];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        wi[k] = make_uint4(0u, 0u, 0u, 0u);
-        if (MODE == 1 || !io || !has[k]) continue;
-        const int qx = x + (k == 2 ? -1 : (k == 3 ? 1 : 0));
-        const int qy = y + (k == 0 ? -1 : (k == 1 ? 1 : 0));
-        const uint8_t *src;
-        if (MODE == 2) {
-            const int px = qx >> 1, py = qy >> 1;
-            src = Mp + m_off(b, (px + py) & 1, k ^ 1, py, px >> 1, g.Hp, g.Wcp, g.Lp) + d0;
-        } else {
-            src = M + m_off(b, colour ^ 1, k ^ 1, qy, qx >> 1, g.H, g.Wc, g.Lp) + d0;
+    for (int k = 0; k < 4; ++k) wi[k] = make_uint4(0u, 0u, 0u, 0u);
+    if (MODE == 0 || MODE == 3) {
+        const uint8_t *Mo = Mb + (size_t)((a.colour ^ 1) * 4u) * P;
+        if (io && has[0]) wi[0] = __ldg(reinterpret_cast<const uint4 *>(Mo + (1u * P + r - rowstep)));
+        if (io && has[1]) wi[1] = __ldg(reinterpret_cast<const uint4 *>(Mo + (r + rowstep)));
+        if (io && has[2]) wi[2] = __ldg(reinterpret_cast<const uint4 *>(Mo + (3u * P + r + (o - 1u) * (uint32_t)a.Lp)));
+        if (io && has[3]) wi[3] = __ldg(reinterpret_cast<const uint4 *>(Mo + (2u * P + r + o * (uint32_t)a.Lp)));
+    } else if (MODE == 2) {
+        const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!io || !has[k]) continue;
+            const int qx = x + (k == 2 ? -1 : (k == 3 ? 1 : 0));
+            const int qy = (int)y + (k == 0 ? -1 : (k == 1 ? 1 : 0));
+            const int px = qx >> 1, py = qy >> 1, slot = k ^ 1;
+            // R-12: the parent's slot toward a missing neighbour counts as 0
+            const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
+            if (!ph) continue;
+            const uint32_t off = ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
+                                 ((uint32_t)py * (uint32_t)a.Wcp + (uint32_t)(px >> 1)) * (uint32_t)a.Lp +
+                                 (uint32_t)d0;
+            wi[k] = __ldg(reinterpret_cast<const uint4 *>(Mpb + off));
         }
-        wi[k] = __ldg(reinterpret_cast<const uint4 *>(src));
     }
-    uint32_t tot[8];
+    uint32_t dv[8];
     if (io) {
-        DLoad<TD>::load(D + d_off(b, colour, y, i, g.H, g.Wc, g.Lp) + d0, tot);
+        DLoad<TD>::load(D + (size_t)b * a.pairD + a.colour * P + r, dv);
     } else {
 #pragma unroll
-        for (int j = 0; j < 8; ++j) tot[j] = 0u;
+        for (int j = 0; j < 8; ++j) dv[j] = 0u;
     }
     uint32_t in[4][8];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        unpack_u8(wi[k], in[k]);
-#pragma unroll
-        for (int j = 0; j < 8; ++j) tot[j] += in[k][j];  // halves < 2^16: no carry
-    }
-    // labels >= L: 0xFFFF halves (excluded from min h, become tau_q after the clamp)
-    uint32_t padm[8];
-    if (PAD) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j)
-            padm[j] = (d0 + j >= g.L ? 0x0000FFFFu : 0u) | (d0 + j + 8 >= g.L ? 0xFFFF0000u : 0u);
-    }
+    for (int k = 0; k < 4; ++k) unpack_u8(wi[k], in[k]);
 
-    // ---- fused WTA (a5): argmin of the belief tot, ties -> smallest d (R-13)
+    // ---- fused WTA (a5): argmin of the belief D + sum of the 4 incoming, ties -> smallest d
     if (WTA) {
         uint32_t best = 0xFFFFFFFFu;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
-            const uint32_t lo = tot[j] & 0xFFFFu, hi = tot[j] >> 16;
-            if (!PAD || d0 + j < g.L) best = min(best, (lo << 9) | (uint32_t)(d0 + j));
-            if (!PAD || d0 + j + 8 < g.L) best = min(best, (hi << 9) | (uint32_t)(d0 + j + 8));
+            const uint32_t tot = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+            const uint32_t lo = tot & 0xFFFFu, hi = tot >> 16;
+            if (!PAD || d0 + j < a.L) best = min(best, (lo << 9) | (uint32_t)(d0 + j));
+            if (!PAD || d0 + j + 8 < a.L) best = min(best, (hi << 9) | (uint32_t)(d0 + j + 8));
         }
-        for (int o = g.G >> 1; o > 0; o >>= 1) best = min(best, __shfl_xor_sync(FULL, best, o, g.G));
-        if (active && lane_g == 0) disp[((size_t)b * g.H + y) * g.W + x] = (int32_t)(best & 511u);
+        for (int s = a.G >> 1; s > 0; s >>= 1) best = min(best, __shfl_xor_sync(FULL, best, s, a.G));
+        if (active && lane_g == 0) a.disp[((size_t)b * a.H + y) * a.W + x] = (int32_t)(best & 511u);
+    }
+    if (MODE == 3) return;
+
+    uint32_t padm[8];
+    if (PAD) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+            padm[j] = (d0 + j >= a.L ? (SIGNED ? 0x00007FFFu : 0x0000FFFFu) : 0u) |
+                      (d0 + j + 8 >= a.L ? (SIGNED ? 0x7FFF0000u : 0xFFFF0000u) : 0u);
     }
 
-    // ---- the four outgoing messages, two directions at a time
+    // ---- the four outgoing messages, two directions at a time:
+    //      h_0 = D + in1+in2+in3, h_1 = D + in0+in2+in3 share D+in2+in3, etc.
 #pragma unroll
     for (int kp = 0; kp < 4; kp += 2) {
         uint32_t h[2][8];
-        uint32_t mn[2];
 #pragma unroll
-        for (int e = 0; e < 2; ++e) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                h[e][j] = tot[j] - in[kp + e][j];
-                if (PAD) h[e][j] |= padm[j];
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t base = kp == 0 ? iadd3(dv[j], in[2][j], in[3][j]) : iadd3(dv[j], in[0][j], in[1][j]);
+            h[0][j] = base + in[kp + 1][j];
+            h[1][j] = base + in[kp][j];
+            if (PAD) {
+                h[0][j] |= padm[j];
+                h[1][j] |= padm[j];
             }
-            const uint32_t a = __vimin3_u16x2(h[e][0], h[e][1], h[e][2]);
-            const uint32_t c = __vimin3_u16x2(h[e][3], h[e][4], h[e][5]);
-            const uint32_t d = __vimin3_u16x2(a, c, __vminu2(h[e][6], h[e][7]));
-            mn[e] = __vminu2(d, prmt(d, 0u, 0x1032));  // min of both halves, in both halves
         }
-        // min over the G lanes of the pixel: direction kp in the low half, kp+1 in the high half
-        uint32_t pm = prmt(mn[0], mn[1], 0x5410);
-        for (int o = g.G >> 1; o > 0; o >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, o, g.G));
-        const uint32_t hm[2] = {prmt(pm, 0u, 0x1010), prmt(pm, 0u, 0x3232)};
+        // min over the G lanes: direction kp in the low half, kp+1 in the high half
+        uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
+        for (int s = a.G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, a.G));
         // h' = min(h - min h, tau_q)
 #pragma unroll
-        for (int e = 0; e < 2; ++e)
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
+            if (SIGNED) {
+                const uint32_t neg = prmt(0u - hm, 0u, 0x1010);  // (-min h) as s16 in both halves
 #pragma unroll
-            for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm[e], TT);
-        // labels d0-1 (from lane-1: its r7 high half) and d0+16 (from lane+1: its r0 low half)
-        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, g.G);
-        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, g.G);
-        if (lane_g == 0) up = TT;
-        if (lane_g == g.G - 1) dn = TT;
+                for (int j = 0; j < 8; ++j) h[e][j] = (uint32_t)__viaddmin_s16x2(h[e][j], neg, a.TT);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
+            }
+        }
+        // labels d0-1 (lane-1's r7 high half) and d0+16 (lane+1's r0 low half)
+        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, a.G);
+        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, a.G);
+        if (lane_g == 0) up = a.TT;
+        if (lane_g == a.G - 1) dn = a.TT;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const int k = kp + e;
             const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);  // (d0-1, d0+7)
             const uint32_t next7 = prmt(h[e][0], dn, e == 0 ? 0x5432 : 0x7632);  // (d0+8, d0+16)
-            uint32_t o[8];
+            uint32_t out[8];
 #pragma unroll
             for (int j = 0; j < 8; ++j) {
                 const uint32_t pv = j == 0 ? prev0 : h[e][j - 1];
                 const uint32_t nx = j == 7 ? next7 : h[e][j + 1];
-                o[j] = __viaddmin_u16x2(pv, SS, __viaddmin_u16x2(nx, SS, h[e][j]));
-                if (PAD) o[j] &= ~padm[j];
-                if (!has[k]) o[j] = 0u;
+                out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[e][j]));
+                if (PAD) out[j] &= ~padm[j];
             }
-            if (io) *reinterpret_cast<uint4 *>(M + m_off(b, colour, k, y, i, g.H, g.Wc, g.Lp) + d0) = pack_u8(o);
+            if (io)
+                *reinterpret_cast<uint4 *>(Mb + ((a.colour * 4u + (uint32_t)(kp + e)) * P + r)) = pack_u8(out);
         }
     }
 }
 
-cudaError_t launch_update_fast(const void *D, int dbytes, void *M, const void *Mp, const Geom &g, int mode, int colour,
-                               int S, int tau_q, int32_t *disp_wta, cudaStream_t st)
+cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
+                               cudaStream_t st)
 {
-    const long threads = (long)g.B * g.H * g.Wc * g.G;
-    const unsigned nb = (unsigned)((threads + 255) / 256);
-    const uint32_t SS = (uint32_t)S | ((uint32_t)S << 16);
-    const uint32_t TT = (uint32_t)tau_q | ((uint32_t)tau_q << 16);
-    const bool pad = (g.L % CH) != 0 || g.G != g.nch;
-    const bool wta = disp_wta != nullptr;
-#define VSBP_FAST(TD_, MODE_, PAD_, WTA_)                                                                        \
-    k_update_fast<TD_, MODE_, PAD_, WTA_><<<nb, 256, 0, st>>>((const TD_ *)D, (uint8_t *)M, (const uint8_t *)Mp, \
-                                                               g, colour, SS, TT, disp_wta)
-#define VSBP_FAST_PW(TD_, MODE_)                                   \
-    if (pad) {                                                     \
-        if (wta) VSBP_FAST(TD_, MODE_, true, true);                \
-        else VSBP_FAST(TD_, MODE_, true, false);                   \
-    } else {                                                       \
-        if (wta) VSBP_FAST(TD_, MODE_, false, true);               \
-        else VSBP_FAST(TD_, MODE_, false, false);                  \
+    const long threads = (long)a.npix * a.G;
+    dim3 grid((unsigned)((threads + 255) / 256), (unsigned)B);
+    const bool pad = (a.L % CH) != 0 || a.G != a.nch;
+#define VSBP_K(TD_, MODE_, PAD_, WTA_, SG_) k_update_fast<TD_, MODE_, PAD_, WTA_, SG_><<<grid, 256, 0, st>>>(a, (const TD_ *)D)
+#define VSBP_S(TD_, MODE_, PAD_, WTA_) \
+    if (sgn) VSBP_K(TD_, MODE_, PAD_, WTA_, true); else VSBP_K(TD_, MODE_, PAD_, WTA_, false);
+#define VSBP_W(TD_, MODE_, PAD_) \
+    if (wta) { VSBP_S(TD_, MODE_, PAD_, true) } else { VSBP_S(TD_, MODE_, PAD_, false) }
+#define VSBP_P(TD_, MODE_) \
+    if (pad) { VSBP_W(TD_, MODE_, true) } else { VSBP_W(TD_, MODE_, false) }
+#define VSBP_M(TD_)                                   \
+    switch (mode) {                                   \
+    case 0: VSBP_P(TD_, 0) break;                     \
+    case 1: VSBP_P(TD_, 1) break;                     \
+    case 2: VSBP_P(TD_, 2) break;                     \
+    default:                                          \
+        if (pad) VSBP_K(TD_, 3, true, true, false);   \
+        else VSBP_K(TD_, 3, false, true, false);      \
+        break;                                        \
     }
-#define VSBP_FAST_M(TD_)                 \
-    if (mode == 0) { VSBP_FAST_PW(TD_, 0) } \
-    else if (mode == 1) { VSBP_FAST_PW(TD_, 1) } \
-    else { VSBP_FAST_PW(TD_, 2) }
     if (dbytes == 1) {
-        VSBP_FAST_M(uint8_t)
+        VSBP_M(uint8_t)
     } else {
-        VSBP_FAST_M(uint16_t)
+        VSBP_M(uint16_t)
     }
-#undef VSBP_FAST_M
-#undef VSBP_FAST_PW
-#undef VSBP_FAST
+#undef VSBP_M
+#undef VSBP_P
+#undef VSBP_W
+#undef VSBP_S
+#undef VSBP_K
     note_launch();
     return cudaGetLastError();
 }

@@ -132,7 +132,12 @@ __global__ void __launch_bounds__(256) k_update(const TD *__restrict__ D, TM *__
         const int slot = k ^ 1;  // up<->down, left<->right
         if (MODE == 2) {
             const int px = qx >> 1, py = qy >> 1;
-            Chunk<TM>::load(Mp + m_off(b, (px + py) & 1, slot, py, px >> 1, g.Hp, g.Wcp, g.Lp) + d0, in[k]);
+            // R-12: the parent's slot toward a missing neighbour counts as 0
+            const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < g.Hp - 1 : slot == 2 ? px > 0 : px < g.Wp - 1;
+            if (ph)
+                Chunk<TM>::load(Mp + m_off(b, (px + py) & 1, slot, py, px >> 1, g.Hp, g.Wcp, g.Lp) + d0, in[k]);
+            else
+                zero16(in[k]);
         } else {
             Chunk<TM>::load(M + m_off(b, oc, slot, qy, qx >> 1, g.H, g.Wc, g.Lp) + d0, in[k]);
         }
@@ -205,9 +210,10 @@ __global__ void __launch_bounds__(256) k_upcopy(TM *__restrict__ M, const TM *__
     const bool has[4] = {y > 0, y < g.H - 1, x > 0, x < g.W - 1};
     const int px = x >> 1, py = y >> 1;
     int v[CH];
+    const bool phas[4] = {py > 0, py < g.Hp - 1, px > 0, px < g.Wp - 1};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-        if (has[k])
+        if (has[k] && phas[k])
             Chunk<TM>::load(Mp + m_off(b, (px + py) & 1, k, py, px >> 1, g.Hp, g.Wcp, g.Lp) + lane_g * CH, v);
         else
             zero16(v);
@@ -287,7 +293,9 @@ __global__ void k_export_msgs(const TM *__restrict__ M, Geom g, int b, int32_t *
         r /= g.W;
         const int y = (int)(r % g.H);
         const int k = (int)(r / g.H);
-        out[t] = (int32_t)M[m_off(b, (x + y) & 1, k, y, x >> 1, g.H, g.Wc, g.Lp) + pos_of_label<TM>(d)];
+        // slots toward missing neighbours are 0 by definition (R-11); the kernels never read them
+        const bool has = k == 0 ? y > 0 : k == 1 ? y < g.H - 1 : k == 2 ? x > 0 : x < g.W - 1;
+        out[t] = has ? (int32_t)M[m_off(b, (x + y) & 1, k, y, x >> 1, g.H, g.Wc, g.Lp) + pos_of_label<TM>(d)] : 0;
     }
 }
 

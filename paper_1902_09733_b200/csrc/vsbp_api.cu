@@ -105,8 +105,50 @@ bool use_fast(const vsbp_bp *c, int l)
 {
     if (c->kernel != 0 || c->msg_bytes != 1 || c->S != 128 || c->tau_q > 255 || c->L > 512) return false;
     if (c->dbytes[l] > 2) return false;
+    if ((long long)8 * c->Hl[l] * c->Wcl[l] * c->Lp >= (1ll << 31)) return false;  // 32-bit offsets per pair
     const long long dmax = ((long long)c->lam_q * c->tau_d) << (2 * l);
     return dmax + 4LL * c->tau_q < 65536LL;
+}
+
+// beliefs of level l fit 15 bits: the signed one-instruction normalise applies
+bool fast_signed(const vsbp_bp *c, int l)
+{
+    const long long dmax = ((long long)c->lam_q * c->tau_d) << (2 * l);
+    return dmax + 4LL * c->tau_q < 32768LL;
+}
+
+vsbp::FastArgs fast_args(const vsbp_bp *c, int l, char *ws, int32_t *disp)
+{
+    vsbp::FastArgs a;
+    const int lp = l + 1 < c->levels ? l + 1 : l;
+    a.M = (uint8_t *)(ws + c->m_off[l]);
+    a.Mp = (const uint8_t *)(ws + c->m_off[lp]);
+    a.disp = disp;
+    a.W = c->Wl[l];
+    a.H = c->Hl[l];
+    a.Wc = c->Wcl[l];
+    a.Wp = c->Wl[lp];
+    a.Hp = c->Hl[lp];
+    a.Wcp = c->Wcl[lp];
+    a.npix = (uint32_t)a.H * (uint32_t)a.Wc;
+    // floor(n / Wc) == umulhi(n, ceil(2^32 / Wc)) for every n < npix when (npix-1) * Wc < 2^32
+    a.magic = 0;
+    if (a.Wc > 1 && (unsigned long long)(a.npix - 1) * (unsigned long long)a.Wc < (1ull << 32))
+        a.magic = (uint32_t)(((1ull << 32) + (unsigned long long)a.Wc - 1) / (unsigned long long)a.Wc);
+    a.L = c->L;
+    a.Lp = c->Lp;
+    a.nch = c->nch;
+    a.G = c->G;
+    a.log2G = c->log2G;
+    a.colour = 0;
+    a.plane = (uint32_t)a.H * (uint32_t)a.Wc * (uint32_t)a.Lp;
+    a.planep = (uint32_t)a.Hp * (uint32_t)a.Wcp * (uint32_t)a.Lp;
+    a.pairD = (size_t)2 * a.plane;
+    a.pairM = (size_t)8 * a.plane;
+    a.pairMp = (size_t)8 * a.planep;
+    a.SS = (uint32_t)c->S | ((uint32_t)c->S << 16);
+    a.TT = (uint32_t)c->tau_q | ((uint32_t)c->tau_q << 16);
+    return a;
 }
 
 }  // namespace
@@ -303,8 +345,10 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         for (int t = 0; t < c->iters; ++t) {
             const int mode = (t > 0) ? 0 : (l == top ? 1 : 2);
             if (fast) {
-                int32_t *wta = (l == 0 && t == c->iters - 1) ? disp : nullptr;  // a5 fused for this colour
-                CK(vsbp::launch_update_fast(D, c->dbytes[l], M, Mp, g, mode, t & 1, c->S, c->tau_q, wta, st));
+                vsbp::FastArgs fa = fast_args(c, l, ws, disp);
+                fa.colour = (uint32_t)(t & 1);
+                const bool wta = (l == 0 && t == c->iters - 1);  // a5 fused for this colour
+                CK(vsbp::launch_update_fast(D, c->dbytes[l], fa, B, mode, wta, fast_signed(c, l), st));
             } else {
                 CK(vsbp::launch_update(D, c->dbytes[l], M, Mp, c->msg_bytes, g, mode, t & 1, c->S, c->tau_q, st));
             }
@@ -322,9 +366,14 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
     }
     // a5 (the colour updated last was labelled inside its update when the fast kernel ran)
     {
-        vsbp::Geom g = geom(c, B, 0);
-        const int only = use_fast(c, 0) ? (((c->iters - 1) & 1) ^ 1) : -1;
-        CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, only, st));
+        if (use_fast(c, 0)) {
+            vsbp::FastArgs fa = fast_args(c, 0, ws, disp);
+            fa.colour = (uint32_t)(((c->iters - 1) & 1) ^ 1);  // the colour not updated last
+            CK(vsbp::launch_update_fast(ws + c->d_off[0], c->dbytes[0], fa, B, 3, true, false, st));
+        } else {
+            vsbp::Geom g = geom(c, B, 0);
+            CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, -1, st));
+        }
     }
     c->last_B = B;
     return VSBP_OK;

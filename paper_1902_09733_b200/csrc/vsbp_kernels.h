@@ -22,8 +22,22 @@ cudaError_t launch_update(const void *D, int dbytes, void *M, const void *Mp, in
 cudaError_t launch_upcopy(void *M, const void *Mp, int mbytes, const Geom &g, int colour, cudaStream_t st);
 cudaError_t launch_wta(const void *D, int dbytes, const void *M, int mbytes, const Geom &g, int32_t *disp,
                        int only_colour, cudaStream_t st);
-cudaError_t launch_update_fast(const void *D, int dbytes, void *M, const void *Mp, const Geom &g, int mode, int colour,
-                               int S, int tau_q, int32_t *disp_wta, cudaStream_t st);
+// arguments of the packed update kernel (bp_fast.cu); offsets are per pair, in elements
+struct FastArgs {
+    uint8_t *M;        // this level's messages
+    const uint8_t *Mp; // parent level's messages (MODE 2)
+    int32_t *disp;     // WTA output (fused WTA / MODE 3)
+    uint32_t npix;     // H * Wc (pixels of one colour)
+    uint32_t magic;    // ceil(2^32 / Wc) when exact for every pixel index, else 0
+    int W, H, Wc, Wp, Hp, Wcp;
+    int L, Lp, nch, G, log2G;
+    uint32_t colour;
+    uint32_t plane, planep;  // H*Wc*Lp, Hp*Wcp*Lp
+    size_t pairD, pairM, pairMp;
+    uint32_t SS, TT;         // S and tau_q replicated in both 16-bit halves
+};
+cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
+                               cudaStream_t st);
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 

@@ -1,0 +1,113 @@
+#!/usr/bin/env python
+"""Summarise ncu outputs (read here, on the CPU box) into a markdown file for profiles/.
+
+  python tools/ncu_summary.py --launches gpurun_out/launches_TAG.csv \
+      --rep gpurun_out/prof_TAG.ncu-rep --out profiles/r01_TAG.md --title "..."
+"""
+from __future__ import annotations
+
+import argparse
+import collections
+import csv
+import io
+import subprocess
+
+KEY_METRICS = [
+    "gpu__time_duration.sum",
+    "dram__bytes_read.sum",
+    "dram__bytes_write.sum",
+    "dram__throughput.avg.pct_of_peak_sustained_elapsed",
+    "lts__t_bytes.sum",
+    "lts__t_sector_hit_rate.pct",
+    "l1tex__t_bytes.sum",
+    "sm__throughput.avg.pct_of_peak_sustained_elapsed",
+    "sm__warps_active.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+    "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+    "smsp__inst_executed.sum",
+    "smsp__issue_active.avg.pct_of_peak_sustained_active",
+    "launch__registers_per_thread",
+    "launch__occupancy_limit_registers",
+    "launch__grid_size",
+    "launch__block_size",
+    "sm__maximum_warps_per_active_cycle_pct",
+    "smsp__warp_issue_stalled_long_scoreboard_per_warp_active.pct",
+    "smsp__warp_issue_stalled_lg_throttle_per_warp_active.pct",
+    "smsp__warp_issue_stalled_wait_per_warp_active.pct",
+    "smsp__warp_issue_stalled_math_pipe_throttle_per_warp_active.pct",
+    "smsp__warp_issue_stalled_short_scoreboard_per_warp_active.pct",
+    "smsp__warp_issue_stalled_barrier_per_warp_active.pct",
+]
+
+
+def launch_table(path):
+    rows = list(csv.reader(open(path)))
+    hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
+    h = rows[hi]
+    ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+    agg = collections.defaultdict(lambda: [0, 0.0])
+    for r in rows[hi + 1:]:
+        if len(r) <= vi:
+            continue
+        name = r[ki].split("(")[0].replace("void ", "")
+        try:
+            v = float(r[vi].replace(",", ""))
+        except ValueError:
+            continue
+        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1e-3)
+        agg[name][0] += 1
+        agg[name][1] += v * scale
+    tot = sum(v[1] for v in agg.values())
+    lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
+    for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
+        lines.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {v[1] / tot:.3f} |")
+    return "\n".join(lines), tot
+
+
+def rep_metrics(path):
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return "(no data)"
+    h, units = rows[0], rows[1]
+    lines = []
+    for rr in rows[2:]:
+        name = rr[h.index("Kernel Name")] if "Kernel Name" in h else "?"
+        lines.append(f"**{name[:120]}**\n")
+        lines.append("| metric | value | unit |")
+        lines.append("|---|---|---|")
+        for m in KEY_METRICS:
+            if m in h:
+                i = h.index(m)
+                lines.append(f"| `{m}` | {rr[i]} | {units[i]} |")
+        lines.append("")
+    return "\n".join(lines)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--launches")
+    ap.add_argument("--rep")
+    ap.add_argument("--out", required=True)
+    ap.add_argument("--title", default="ncu summary")
+    ap.add_argument("--notes", default="")
+    a = ap.parse_args()
+    parts = [f"# {a.title}\n"]
+    if a.notes:
+        parts.append(a.notes + "\n")
+    if a.launches:
+        t, tot = launch_table(a.launches)
+        parts.append("## Launch list (ncu `gpu__time_duration.sum`, cold-cache, serialised)\n")
+        parts.append(f"Total device time of the captured launches: {tot:.1f} us\n")
+        parts.append(t + "\n")
+    if a.rep:
+        parts.append("## `--set full` capture of the top kernel\n")
+        parts.append(rep_metrics(a.rep) + "\n")
+    with open(a.out, "w") as f:
+        f.write("\n".join(parts))
+    print(open(a.out).read())
+
+
+if __name__ == "__main__":
+    main()
