@@ -85,10 +85,31 @@ def rep_metrics(path):
     return "\n".join(lines)
 
 
+def rep_traffic(path):
+    """{short kernel name: dram__bytes_read.sum + dram__bytes_write.sum} in bytes"""
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return {}
+    h, units = rows[0], rows[1]
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    res = {}
+    for rr in rows[2:]:
+        name = rr[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+        tot = 0.0
+        for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+            i = h.index(m)
+            tot += float(rr[i].replace(",", "")) * scale.get(units[i], 1.0)
+        res[name] = tot
+    return res
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--launches")
-    ap.add_argument("--rep")
+    ap.add_argument("--rep", action="append", default=[])
+    ap.add_argument("--traffic-json", help="write {kernel: dram bytes per launch} for bench.py's roofline.traffic")
+    ap.add_argument("--batch", type=int, default=0, help="pairs per launch of the captured run")
     ap.add_argument("--out", required=True)
     ap.add_argument("--title", default="ncu summary")
     ap.add_argument("--notes", default="")
@@ -101,9 +122,15 @@ def main():
         parts.append("## Launch list (ncu `gpu__time_duration.sum`, cold-cache, serialised)\n")
         parts.append(f"Total device time of the captured launches: {tot:.1f} us\n")
         parts.append(t + "\n")
-    if a.rep:
-        parts.append("## `--set full` capture of the top kernel\n")
-        parts.append(rep_metrics(a.rep) + "\n")
+    traffic = {}
+    for rep in a.rep:
+        parts.append("## `--set full` capture\n")
+        parts.append(rep_metrics(rep) + "\n")
+        traffic.update(rep_traffic(rep))
+    if a.traffic_json:
+        import json
+        with open(a.traffic_json, "w") as f:
+            json.dump({"batch": a.batch, "source": a.out, "dram_bytes_per_launch": traffic}, f, indent=1)
     with open(a.out, "w") as f:
         f.write("\n".join(parts))
     print(open(a.out).read())
