@@ -54,6 +54,7 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
+    p.add_argument("--cpu-pairs", type=int, default=4, help="oracle pairs per host thread (cpu_baseline)")
     return p.parse_args()
 
 
@@ -136,6 +137,22 @@ def q_intrinsics():
     import synthgen
     I = synthgen.INTRINSICS
     return I
+
+
+def ncu_traffic(batch: int):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of the level-0 message
+    update, from the committed `ncu --set full` capture (profiles/traffic.json),
+    when that capture was taken at this batch size; else None."""
+    path = os.path.join(ROOT, "profiles", "traffic.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if int(d.get("batch", -1)) != batch:
+        return None
+    v = d.get("dram_bytes_per_launch", {}).get(d.get("dominant", ""))
+    return float(v) if v is not None else None
 
 
 # ----------------------------------------------------------------------------- oracle timing
@@ -307,7 +324,7 @@ def run_ours(args):
     roofline = {
         "kernel": "k_update (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
         "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": None,
+        "traffic": ncu_traffic(B),
         "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
         "us_per_launch": 1000.0 * l0["ms"] / max(l0["launches"], 1),
         "share_of_step": all_ms / (ms if ms > 0 else 1.0),
@@ -318,7 +335,7 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or default_threads()
-        v, n, dt = oracle_rate(threads, 1, lpool, rpool)
+        v, n, dt = oracle_rate(threads, args.cpu_pairs, lpool, rpool)
         cpu = {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
                "sample": f"{n} pairs of the same workload, one per host thread ({dt:.1f} s)"}
 
