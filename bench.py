@@ -9,7 +9,7 @@ of synthetic 2.7K RGB virtual-stereo pairs; one step = one batch of B pairs per
 GPU through the whole path: prep (s=4) -> hierarchical BP 676x380, L=64, 5 levels
 x 5 iterations -> JBU r=2 to 2704x1520 -> reprojection -> per-pair summary, then
 an NCCL all_gather of the summaries (the only exchange).  Pairs are
-sharded round-robin (pair i -> rank i mod N): weak scaling.
+sharded round-robin by batch (batch k of B pairs -> rank k mod N, shard.py): weak scaling.
 
 `value`  : pairs/s over all ranks, inputs resident in HBM, device-timed (CUDA
            events on the launching stream, max over ranks).
@@ -223,6 +223,7 @@ def run_ours(args):
     import torch.distributed as dist
 
     import paper_1902_09733_b200 as P
+    from paper_1902_09733_b200 import shard
 
     rank, world, local = dist_env()
     if world != args.gpus:
@@ -238,7 +239,7 @@ def run_ours(args):
     pipe = P.StereoPipeline(W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS, batch=B, Q=Q, device=dev)
     pipe.bp.timing(True)
 
-    # seeded synthetic pairs; rank r owns pairs i = r, r+N, ... (round-robin shard)
+    # seeded synthetic pairs; rank r owns global batches r, r+N, ... (shard.py)
     pool_n = max(1, min(args.pool, B))
     lpool, rpool = make_pool(7000 + 100 * rank, pool_n)
     idx = [i % pool_n for i in range(B)]
@@ -250,12 +251,8 @@ def run_ours(args):
     stream = torch.cuda.current_stream(dev)
 
     def step(s, lt, rt):
-        first = (s * world + rank) * B
-        summ = pipe.run(lt, rt, first_pair_id=first)
-        if world > 1:
-            dist.all_gather_into_tensor(gathered, summ)
-        else:
-            gathered.copy_(summ)
+        summ = pipe.run(lt, rt, first_pair_id=shard.batch_first_pair(s, rank, world, B))
+        shard.gather_summaries(summ, out=gathered)  # the one exchange
         return summ
 
     def barrier():
@@ -304,8 +301,9 @@ def run_ours(args):
         barrier()
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        gather = (lambda summ: dist.all_gather_into_tensor(gathered, summ)) if world > 1 else None
-        runner.run([(left_h, right_h)] * args.steps, first_pair_id=rank * B, gather=gather)
+        gather = (lambda summ: shard.gather_summaries(summ, out=gathered)) if world > 1 else None
+        runner.run([(left_h, right_h)] * args.steps, first_pair_id=shard.batch_first_pair(0, rank, world, B),
+                   pair_stride=world * B, gather=gather)
         f1.record(stream)
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1))

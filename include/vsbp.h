@@ -70,7 +70,9 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *   VSBP_OPT_MSG_BYTES : message storage width in bytes, 0 = narrowest lossless
  *                        (u8 if tau_q <= 255, u16 if <= 65535, else 4), 1, 2 or 4;
  *                        narrower than lossless -> VSBP_EINVAL.
- *   VSBP_OPT_KERNEL    : 0 = fastest available message kernel, 1 = generic. */
+ *   VSBP_OPT_KERNEL    : 0 = fastest available kernels (packed message update,
+ *                        fused cost volume + pyramid), 1 = generic kernels
+ *                        (same results, bit for bit). */
 #define VSBP_OPT_MSG_BYTES 1
 #define VSBP_OPT_KERNEL 2
 int bp_set_option(vsbp_bp *ctx, int option, int value);

@@ -354,11 +354,14 @@ class StereoStream:
         self.summary_host = torch.empty((B, 8), dtype=torch.int64).pin_memory()
         self.device = dev
 
-    def run(self, batches, first_pair_id: int = 0, gather=None, on_summary=None):
+    def run(self, batches, first_pair_id: int = 0, gather=None, on_summary=None, pair_stride: int | None = None):
         """batches: iterable of (left_host, right_host) pinned uint8 [B,H,W,3].
         Enqueues everything; returns the number of batches.  gather(summary) is
         called on the compute stream after every batch (e.g. the NCCL all_gather of
-        the summaries); on_summary(i, host tensor) after a final synchronise."""
+        the summaries); on_summary(i, host tensor) after a final synchronise.
+        Batch i's pairs are numbered first_pair_id + i*pair_stride + j (pair_stride
+        defaults to B; a rank of N uses N*B, shard.batch_first_pair)."""
+        stride = self.pipe.B if pair_stride is None else pair_stride
         compute = torch.cuda.current_stream(self.device)
         n = 0
         for i, (lh, rh) in enumerate(batches):
@@ -370,7 +373,7 @@ class StereoStream:
                 rd.copy_(rh, non_blocking=True)
                 self.copied[k].record(self.copy_stream)
             compute.wait_event(self.copied[k])
-            summ = self.pipe.run(ld, rd, first_pair_id=first_pair_id + i * self.pipe.B)
+            summ = self.pipe.run(ld, rd, first_pair_id=first_pair_id + i * stride)
             self.freed[k].record(compute)
             if gather is not None:
                 gather(summ)

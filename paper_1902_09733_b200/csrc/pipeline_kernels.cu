@@ -33,6 +33,39 @@ __global__ void __launch_bounds__(256) k_prep(const uint8_t *__restrict__ rgb, i
     gray[t] = (uint8_t)((sum + n2 / 2) / n2);
 }
 
+// s % 4 == 0: each footprint row is 3s/4 aligned 32-bit words (W_hi % 4 == 0 and the
+// frame size is a multiple of 4), read as words; a warp's 32 pixels read
+// contiguous 12s-byte runs per row.  Same arithmetic as k_prep.
+template <int S4>
+__global__ void __launch_bounds__(256) k_prep_w(const uint8_t *__restrict__ rgb, int W_hi, int H_hi, int n,
+                                                uint8_t *__restrict__ gray)
+{
+    constexpr int s = 4 * S4, NW = 3 * S4;  // words per footprint row
+    const int W = W_hi / s, H = H_hi / s;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)n * W * H) return;
+    const int f = (int)(t / ((long)W * H));
+    const long r = t - (long)f * W * H;
+    const int Y = (int)(r / W), X = (int)(r - (long)Y * W);
+    const uint8_t *base = rgb + (size_t)f * H_hi * W_hi * 3;
+    int sum = 0;
+#pragma unroll
+    for (int j = 0; j < s; ++j) {
+        const unsigned *row = reinterpret_cast<const unsigned *>(base + ((size_t)(Y * s + j) * W_hi + (size_t)X * s) * 3);
+        unsigned w[NW];
+#pragma unroll
+        for (int q = 0; q < NW; ++q) w[q] = __ldg(row + q);
+#pragma unroll
+        for (int i = 0; i < s; ++i) {
+            const int R = (w[(3 * i) >> 2] >> (8 * ((3 * i) & 3))) & 0xff;
+            const int G = (w[(3 * i + 1) >> 2] >> (8 * ((3 * i + 1) & 3))) & 0xff;
+            const int Bc = (w[(3 * i + 2) >> 2] >> (8 * ((3 * i + 2) & 3))) & 0xff;
+            sum += (77 * R + 150 * G + 29 * Bc + 128) >> 8;
+        }
+    }
+    gray[t] = (uint8_t)((sum + s * s / 2) / (s * s));
+}
+
 // ======================================================================== a7
 struct QMat {
     float q[16];
@@ -130,7 +163,13 @@ __global__ void __launch_bounds__(256) k_summary(const int32_t *__restrict__ dis
 cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray, cudaStream_t st)
 {
     const long threads = (long)n * (W_hi / s) * (H_hi / s);
-    k_prep<<<(unsigned)((threads + 255) / 256), 256, 0, st>>>(rgb, W_hi, H_hi, s, n, gray);
+    const unsigned nb = (unsigned)((threads + 255) / 256);
+    if (s == 4 && ((uintptr_t)rgb & 3) == 0)
+        k_prep_w<1><<<nb, 256, 0, st>>>(rgb, W_hi, H_hi, n, gray);
+    else if (s == 8 && ((uintptr_t)rgb & 3) == 0)
+        k_prep_w<2><<<nb, 256, 0, st>>>(rgb, W_hi, H_hi, n, gray);
+    else
+        k_prep<<<nb, 256, 0, st>>>(rgb, W_hi, H_hi, s, n, gray);
     note_launch();
     return cudaGetLastError();
 }

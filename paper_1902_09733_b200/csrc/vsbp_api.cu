@@ -312,12 +312,34 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
     plan(c, c->ws_batch);
     char *ws = wsp(c);
     const int top = c->levels - 1;
-    // a1: cost volume, a2: pyramid
-    {
+    // a1: cost volume, a2: pyramid -- fused for the first F levels when the
+    // tile's shared memory fits (costpyr.cu), the rest level by level
+    int l_from = 0;
+    const int F = c->levels < 5 ? c->levels : 5;
+    if (c->kernel == 0 && vsbp::costpyr_smem(c->L, c->Lp, F) <= 160 * 1024) {
+        vsbp::CostPyrArgs a;
+        memset(&a, 0, sizeof a);
+        for (int l = 0; l < F; ++l) {
+            a.D[l] = ws + c->d_off[l];
+            a.dbytes[l] = c->dbytes[l];
+            a.W[l] = c->Wl[l];
+            a.H[l] = c->Hl[l];
+            a.Wc[l] = c->Wcl[l];
+            a.pairD[l] = (size_t)2 * c->Hl[l] * c->Wcl[l] * c->Lp;
+        }
+        a.L = c->L;
+        a.Lp = c->Lp;
+        a.nch = c->nch;
+        a.F = F;
+        a.lam_q = c->lam_q;
+        a.tau_d = c->tau_d;
+        CK(vsbp::launch_costpyr(left, right, a, B, st));
+        l_from = F - 1;
+    } else {
         vsbp::Geom g = geom(c, B, 0);
         CK(vsbp::launch_costvol(left, right, ws + c->d_off[0], c->dbytes[0], g, c->lam_q, c->tau_d, st));
     }
-    for (int l = 0; l < top; ++l) {
+    for (int l = l_from; l < top; ++l) {
         vsbp::Geom g = geom(c, B, l);
         CK(vsbp::launch_pyramid(ws + c->d_off[l], c->dbytes[l], ws + c->d_off[l + 1], c->dbytes[l + 1], g, st));
     }

@@ -16,6 +16,18 @@ struct Geom {
 
 cudaError_t launch_costvol(const uint8_t *left, const uint8_t *right, void *D, int dbytes, const Geom &g, int lam_q,
                            int tau_d, cudaStream_t st);
+// fused cost volume + pyramid levels 0..F-1 (costpyr.cu), F <= 5
+struct CostPyrArgs {
+    void *D[5];
+    int dbytes[5];
+    int W[5], H[5], Wc[5];
+    size_t pairD[5];  // elements per pair of level l's cost array
+    int L, Lp, nch, F;
+    int lam_q, tau_d;
+    int img_smem;     // set by the launcher
+};
+size_t costpyr_smem(int L, int Lp, int F);
+cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArgs a, int B, cudaStream_t st);
 cudaError_t launch_pyramid(const void *Dc, int cbytes, void *Dp, int pbytes, const Geom &g, cudaStream_t st);
 cudaError_t launch_update(const void *D, int dbytes, void *M, const void *Mp, int mbytes, const Geom &g, int mode,
                           int colour, int S, int tau_q, cudaStream_t st);

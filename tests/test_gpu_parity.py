@@ -100,6 +100,27 @@ def test_wide_tau_q_u16_and_i32_storage():
     check_bp_case(l, r, 24, 2, 3, lam=2.0, dt=60.0, st=1000.0)    # tau_q = 128000 -> i32
 
 
+@pytest.mark.parametrize("W,H,L,levels", [(97, 61, 32, 4), (70, 41, 130, 6), (9, 17, 64, 5)])
+def test_generic_and_fused_kernels_agree_with_oracle(W, H, L, levels):
+    """VSBP_OPT_KERNEL=1 (separate cost-volume, pyramid and generic update kernels)
+    and the default fused/packed kernels both reproduce the oracle bit for bit."""
+    rng = np.random.default_rng(W + H + L)
+    l = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    d_o, msgs_o = oracle.bp_disparity(l, r, L, levels, 5, return_messages=True)
+    D = oracle.cost_volume(l, r, L, oracle.quantize(0.07, 15.0, 1.7))
+    for kernel in (0, 1):
+        bp = P.StereoBP(W, H, L, levels, 5, kernel=kernel, device=dev())
+        disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+        assert np.array_equal(disp, d_o)
+        Dl = D
+        for lv in range(levels):
+            assert np.array_equal(bp.costs(0, lv).cpu().numpy(), Dl), f"kernel {kernel} costs level {lv}"
+            assert np.array_equal(bp.messages(0, lv).cpu().numpy(), msgs_o[lv])
+            if lv + 1 < levels:
+                Dl = oracle.pyramid_down(Dl)
+
+
 def test_batch_equals_single():
     pairs = [synthgen.shifted_pair(10 + i, 80, 50, 3 + i) for i in range(3)]
     left = np.stack([p[0] for p in pairs])
@@ -157,7 +178,8 @@ def test_prep_full_frame_batch():
 
 # ----------------------------------------------------------------------------- a6
 @pytest.mark.parametrize("s,r,ss,sr", [(2, 1, 1.3, 40.0), (3, 2, 2.0, 20.0), (4, 2, 3.75, 15.0), (4, 5, 3.75, 15.0),
-                                       (2, 3, 7.5, 15.0), (1, 4, 2.0, 30.0), (5, 3, 3.0, 8.0)])
+                                       (2, 3, 7.5, 15.0), (1, 4, 2.0, 30.0), (5, 3, 3.0, 8.0), (8, 1, 7.5, 15.0),
+                                       (6, 2, 5.0, 15.0)])
 def test_jbu_small(s, r, ss, sr):
     rng = np.random.default_rng(s * 10 + r)
     lo = rng.integers(0, 64, size=(13, 19)).astype(np.int32)
@@ -177,6 +199,21 @@ def test_jbu_adversarial_colours():
     got = P.jbu_upsample(to_dev(lo), to_dev(guide), s, 3.75, 15.0, r).cpu().numpy().astype(np.float64)
     ref = oracle.jbu(lo, guide, s, 3.75, 15.0, r)
     assert np.max(np.abs(got - ref)) <= 1e-4
+
+
+@pytest.mark.parametrize("s,r", [(4, 2), (2, 3), (8, 1), (4, 5)])
+def test_jbu_vector_path_equals_scalar_path(s, r):
+    """The P-pixels-per-thread kernel (s % P == 0, aligned buffers) and the one-pixel
+    kernel (chosen when the output is misaligned) compute the same f32 arithmetic in
+    the same order: bit-identical outputs."""
+    rng = np.random.default_rng(5 * s + r)
+    H, W = 21, 37
+    lo = to_dev(rng.integers(0, 48, size=(H, W)).astype(np.int32))
+    guide = to_dev(synthgen.value_noise_rgb(s * r, W * s, H * s))
+    vec = P.jbu_upsample(lo, guide, s, 3.75, 15.0, r)
+    buf = torch.empty(H * s * W * s + 1, dtype=torch.float32, device=dev())
+    sca = P.jbu_upsample(lo, guide, s, 3.75, 15.0, r, out=buf[1:].view(1, H * s, W * s))
+    assert torch.equal(vec, sca)
 
 
 def test_jbu_full_frame_config3():

@@ -42,26 +42,41 @@ KEY_METRICS = [
 
 
 def launch_table(path):
+    """Per-kernel launches, device time (gpu__time_duration.sum) and, when the CSV
+    carries them, DRAM bytes (dram__bytes_read.sum + dram__bytes_write.sum)."""
     rows = list(csv.reader(open(path)))
     hi = next(i for i, r in enumerate(rows) if "Kernel Name" in r)
     h = rows[hi]
     ki, vi, ui = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
-    agg = collections.defaultdict(lambda: [0, 0.0])
+    mi = h.index("Metric Name") if "Metric Name" in h else None
+    tscale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
+    bscale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    agg = collections.defaultdict(lambda: [0, 0.0, 0.0])
     for r in rows[hi + 1:]:
         if len(r) <= vi:
             continue
         name = r[ki].split("(")[0].replace("void ", "")
+        metric = r[mi] if mi is not None else "gpu__time_duration.sum"
         try:
             v = float(r[vi].replace(",", ""))
         except ValueError:
             continue
-        scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}.get(r[ui], 1e-3)
-        agg[name][0] += 1
-        agg[name][1] += v * scale
+        if metric == "gpu__time_duration.sum":
+            agg[name][0] += 1
+            agg[name][1] += v * tscale.get(r[ui], 1e-3)
+        elif metric.startswith("dram__bytes"):
+            agg[name][2] += v * bscale.get(r[ui], 1.0)
     tot = sum(v[1] for v in agg.values())
-    lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
+    has_b = any(v[2] > 0 for v in agg.values())
+    if has_b:
+        lines = ["| kernel | launches | total us | share | DRAM MB per launch | DRAM GB/s |", "|---|---|---|---|---|---|"]
+    else:
+        lines = ["| kernel | launches | total us | share |", "|---|---|---|---|"]
     for k, v in sorted(agg.items(), key=lambda x: -x[1][1]):
-        lines.append(f"| `{k}` | {v[0]} | {v[1]:.1f} | {v[1] / tot:.3f} |")
+        row = f"| `{k}` | {v[0]} | {v[1]:.1f} | {v[1] / tot:.3f} |"
+        if has_b:
+            row += f" {v[2] / max(v[0], 1) / 1e6:.1f} | {v[2] / 1e3 / v[1] if v[1] > 0 else 0:.0f} |"
+        lines.append(row)
     return "\n".join(lines), tot
 
 
