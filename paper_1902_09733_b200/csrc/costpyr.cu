@@ -31,6 +31,56 @@ __device__ __forceinline__ void store_chunk(void *base, int bytes, size_t off, c
         Chunk<int32_t>::store((int32_t *)base + off, v);
 }
 
+// levels 2..F-1 (a2) from the previous level's int32 chunks in shared memory
+__device__ __forceinline__ void upper_levels(const CostPyrArgs &a, int *sD, int X0, int Y0, int b)
+{
+    const int Lp = a.Lp, nch = a.nch;
+    int *prev = sD;
+    int Tp = CP_T / 2;
+    for (int l = 2; l < a.F; ++l) {
+        __syncthreads();
+        const int T = Tp >> 1;
+        int *cur = prev + (size_t)Tp * Tp * Lp;
+        const int Wl = a.W[l], Hl = a.H[l], Wcl = a.Wc[l];
+        const int Wc_ = a.W[l - 1], Hc_ = a.H[l - 1];
+        const int Xl = X0 >> l, Yl = Y0 >> l;
+        for (int it = threadIdx.x; it < T * T * nch; it += blockDim.x) {
+            const int p = it / nch, k = it - p * nch;
+            const int px = p % T, py = p / T;
+            const int X = Xl + px, Y = Yl + py;
+            int v[CH];
+            zero16(v);
+            if (X < Wl && Y < Hl) {
+#pragma unroll
+                for (int jy = 0; jy < 2; ++jy)
+#pragma unroll
+                    for (int jx = 0; jx < 2; ++jx) {
+                        if (2 * X + jx >= Wc_ || 2 * Y + jy >= Hc_) continue;
+                        const int4 *src =
+                            reinterpret_cast<const int4 *>(prev + (size_t)((2 * py + jy) * Tp + 2 * px + jx) * Lp + k * CH);
+#pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const int4 w = src[u];
+                            v[4 * u] += w.x;
+                            v[4 * u + 1] += w.y;
+                            v[4 * u + 2] += w.z;
+                            v[4 * u + 3] += w.w;
+                        }
+                    }
+                store_chunk(a.D[l], a.dbytes[l],
+                            (size_t)b * a.pairD[l] + d_off(0, (X + Y) & 1, Y, X >> 1, Hl, Wcl, Lp) + k * CH, v);
+            }
+            if (l + 1 < a.F) {
+                int4 *dst = reinterpret_cast<int4 *>(cur + (size_t)p * Lp + k * CH);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) dst[u] = make_int4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            }
+        }
+        prev = cur;
+        Tp = T;
+    }
+}
+
 __global__ void __launch_bounds__(256) k_costpyr(const uint8_t *__restrict__ left, const uint8_t *__restrict__ right,
                                                  CostPyrArgs a)
 {
@@ -101,72 +151,183 @@ __global__ void __launch_bounds__(256) k_costpyr(const uint8_t *__restrict__ lef
         }
     }
 
-    // ---- levels 2..F-1 (a2) from the previous level in shared memory
-    int *prev = sD;
-    int Tp = TQ;
-    for (int l = 2; l < a.F; ++l) {
-        __syncthreads();
-        const int T = Tp >> 1;
-        int *cur = prev + (size_t)Tp * Tp * Lp;
-        const int Wl = a.W[l], Hl = a.H[l], Wcl = a.Wc[l];
-        const int Wc_ = a.W[l - 1], Hc_ = a.H[l - 1];
-        const int Xl = X0 >> l, Yl = Y0 >> l;
-        for (int it = threadIdx.x; it < T * T * nch; it += blockDim.x) {
-            const int p = it / nch, k = it - p * nch;
-            const int px = p % T, py = p / T;
-            const int X = Xl + px, Y = Yl + py;
-            int v[CH];
-            zero16(v);
-            if (X < Wl && Y < Hl) {
+    upper_levels(a, sD, X0, Y0, b);
+}
+
+// ---------------------------------------------------------------- packed fast path
+// Same values as k_costpyr, for parameters where every level-0 cost and every
+// level-1 sum fits 16 bits (host check costpyr_fast_ok).  Two labels per 32-bit
+// register as s16x2 on the DPX datapath, in the chunk order of vsbp_internal.cuh:
+// r_j = (label 16k+j | label 16k+j+8 << 16), which is the u16 storage word j and
+// one PRMT away from the u8 storage.  The staged right row holds, per column i,
+// the pair (R(i), R(i-8)) as s16x2, so for a pixel with grey l
+//   min(|l - r|, tau_d) = max(min((l+1) + ~r, tau_d), min(-l + r, tau_d))
+// (~r = -r-1 per half) is a LOP3, two VIADDMNMX and a VIMNMX per label pair, and
+// the data weight one IMAD of the packed pair.  The two pixels of a quad row share
+// 9 of their 16 column reads.  Columns left of the image hold r = -2048: both mins
+// give tau_d there, i.e. the border cost lambda_q * tau_d (R-8).
+constexpr int CPF_SENT = -2048;
+
+__device__ __forceinline__ uint32_t cp_prmt(uint32_t a, uint32_t b, uint32_t sel)
+{
+    uint32_t r;
+    asm("prmt.b32 %0, %1, %2, %3;" : "=r"(r) : "r"(a), "r"(b), "r"(sel));
+    return r;
+}
+
+__device__ __forceinline__ void store_pairs(void *base, int bytes, size_t off, const uint32_t r[8])
+{
+    if (bytes == 1) {
+        uint32_t u[4];
 #pragma unroll
-                for (int jy = 0; jy < 2; ++jy)
+        for (int q = 0; q < 4; ++q) u[q] = cp_prmt(r[2 * q], r[2 * q + 1], 0x6240);
+        *reinterpret_cast<uint4 *>((uint8_t *)base + off) = make_uint4(u[0], u[1], u[2], u[3]);
+    } else {
+        uint4 *d = reinterpret_cast<uint4 *>((uint16_t *)base + off);
+        d[0] = make_uint4(r[0], r[1], r[2], r[3]);
+        d[1] = make_uint4(r[4], r[5], r[6], r[7]);
+    }
+}
+
+template <bool PAD>
+__global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict__ left,
+                                                      const uint8_t *__restrict__ right, CostPyrArgs a)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const int b = blockIdx.z;
+    const int X0 = blockIdx.x * CP_T, Y0 = blockIdx.y * CP_T;
+    const int L = a.L, Lp = a.Lp, nch = a.nch;
+    const int W = a.W[0], H = a.H[0];
+    const int span = Lp + CP_T - 9;        // columns i = X0-Lp+9 .. X0+15
+    const int i0 = X0 - Lp + 9;
+    uint8_t *sl = smem;                     // [16][16]
+    uint32_t *sr = reinterpret_cast<uint32_t *>(smem + CP_T * CP_T);  // [16][span]: (R(i), R(i-8)) as s16x2
+    int *sD = reinterpret_cast<int *>(smem + a.img_smem);
+    const uint8_t *lb = left + (size_t)b * H * W;
+    const uint8_t *rb = right + (size_t)b * H * W;
+    for (int e = threadIdx.x; e < CP_T * CP_T; e += blockDim.x) {
+        const int x = X0 + (e & (CP_T - 1)), y = Y0 + e / CP_T;
+        sl[e] = (x < W && y < H) ? __ldg(lb + (size_t)y * W + x) : 0;
+    }
+    for (int e = threadIdx.x; e < CP_T * span; e += blockDim.x) {
+        const int r = e / span, j = e - r * span;
+        const int i = i0 + j, y = Y0 + r;
+        int v0 = 0, v1 = 0;
+        if (y < H) {
+            v0 = i < 0 ? CPF_SENT : (i < W ? (int)__ldg(rb + (size_t)y * W + i) : 0);
+            v1 = i - 8 < 0 ? CPF_SENT : (i - 8 < W ? (int)__ldg(rb + (size_t)y * W + i - 8) : 0);
+        }
+        sr[e] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
+    }
+    __syncthreads();
+
+    const uint32_t T2 = (uint32_t)a.tau_d | ((uint32_t)a.tau_d << 16);
+    const uint32_t lam = (uint32_t)a.lam_q;
+    constexpr int TQ = CP_T / 2;
+    for (int it = threadIdx.x; it < TQ * TQ * nch; it += blockDim.x) {
+        const int q = it / nch, k = it - q * nch;
+        const int qx = q % TQ, qy = q / TQ;
+        uint32_t mask[8];
 #pragma unroll
-                    for (int jx = 0; jx < 2; ++jx) {
-                        if (2 * X + jx >= Wc_ || 2 * Y + jy >= Hc_) continue;
-                        const int4 *src =
-                            reinterpret_cast<const int4 *>(prev + (size_t)((2 * py + jy) * Tp + 2 * px + jx) * Lp + k * CH);
+        for (int j = 0; j < 8; ++j)
+            mask[j] = PAD ? ((k * CH + j < L ? 0x0000FFFFu : 0u) | (k * CH + j + 8 < L ? 0xFFFF0000u : 0u)) : ~0u;
+        uint32_t acc[8];
 #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const int4 w = src[u];
-                            v[4 * u] += w.x;
-                            v[4 * u + 1] += w.y;
-                            v[4 * u + 2] += w.z;
-                            v[4 * u + 3] += w.w;
-                        }
-                    }
-                store_chunk(a.D[l], a.dbytes[l],
-                            (size_t)b * a.pairD[l] + d_off(0, (X + Y) & 1, Y, X >> 1, Hl, Wcl, Lp) + k * CH, v);
+        for (int j = 0; j < 8; ++j) acc[j] = 0u;
+#pragma unroll
+        for (int jy = 0; jy < 2; ++jy) {
+            const int py = 2 * qy + jy, y = Y0 + py;
+            if (y >= H) continue;
+            // columns x0q+1-16k-jj, jj = 0..8: pixel jx=1 uses jj = j, pixel jx=0 uses jj = j+1
+            const uint32_t *col = sr + py * span + (X0 + 2 * qx + 1 - k * CH - i0);
+            uint32_t e[9], ne[9];
+#pragma unroll
+            for (int jj = 0; jj < 9; ++jj) {
+                e[jj] = col[-jj];
+                ne[jj] = ~e[jj];
             }
-            if (l + 1 < a.F) {
-                int4 *dst = reinterpret_cast<int4 *>(cur + (size_t)p * Lp + k * CH);
 #pragma unroll
-                for (int u = 0; u < 4; ++u) dst[u] = make_int4(v[4 * u], v[4 * u + 1], v[4 * u + 2], v[4 * u + 3]);
+            for (int jx = 0; jx < 2; ++jx) {
+                const int px = 2 * qx + jx, x = X0 + px;
+                if (x >= W) continue;
+                const uint32_t lv = sl[py * CP_T + px];
+                const uint32_t lp1 = (lv + 1u) * 0x00010001u;
+                const uint32_t nl2 = ((0u - lv) & 0xFFFFu) * 0x00010001u;
+                uint32_t r[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const int jj = j + 1 - jx;
+                    const uint32_t lo = __viaddmin_s16x2(lp1, ne[jj], T2);  // min(l - r, tau_d)
+                    const uint32_t hi = __viaddmin_s16x2(nl2, e[jj], T2);   // min(r - l, tau_d)
+                    r[j] = __vmaxs2(lo, hi) * lam;
+                    if (PAD) r[j] &= mask[j];
+                    acc[j] += r[j];
+                }
+                store_pairs(a.D[0], a.dbytes[0],
+                            (size_t)b * a.pairD[0] + d_off(0, (x + y) & 1, y, x >> 1, H, a.Wc[0], Lp) + k * CH, r);
             }
         }
-        prev = cur;
-        Tp = T;
+        if (a.F > 1) {
+            const int X = (X0 >> 1) + qx, Y = (Y0 >> 1) + qy;
+            if (X < a.W[1] && Y < a.H[1])
+                store_pairs(a.D[1], a.dbytes[1],
+                            (size_t)b * a.pairD[1] + d_off(0, (X + Y) & 1, Y, X >> 1, a.H[1], a.Wc[1], Lp) + k * CH,
+                            acc);
+            if (a.F > 2) {
+                int4 *dst = reinterpret_cast<int4 *>(sD + (size_t)q * Lp + k * CH);
+                dst[0] = make_int4(acc[0] & 0xFFFF, acc[1] & 0xFFFF, acc[2] & 0xFFFF, acc[3] & 0xFFFF);
+                dst[1] = make_int4(acc[4] & 0xFFFF, acc[5] & 0xFFFF, acc[6] & 0xFFFF, acc[7] & 0xFFFF);
+                dst[2] = make_int4(acc[0] >> 16, acc[1] >> 16, acc[2] >> 16, acc[3] >> 16);
+                dst[3] = make_int4(acc[4] >> 16, acc[5] >> 16, acc[6] >> 16, acc[7] >> 16);
+            }
+        }
     }
+    upper_levels(a, sD, X0, Y0, b);
+}
+
+bool costpyr_fast_ok(const CostPyrArgs &a)
+{
+    const long long lt = (long long)a.lam_q * a.tau_d;
+    if (a.tau_d > 1000 || a.dbytes[0] > 2 || lt > 65535) return false;
+    if (a.F > 1 && (a.dbytes[1] > 2 || 4 * lt > 65535)) return false;
+    return true;
+}
+
+static size_t img_bytes(int L, int Lp)
+{
+    const size_t generic = (size_t)CP_T * CP_T + (size_t)CP_T * (CP_T + L - 1);
+    const size_t fast = (size_t)CP_T * CP_T + (size_t)CP_T * (Lp + CP_T - 9) * 4;
+    const size_t m = generic > fast ? generic : fast;
+    return (m + 15) & ~(size_t)15;
 }
 
 size_t costpyr_smem(int L, int Lp, int F)
 {
-    const size_t img = (size_t)CP_T * CP_T + (size_t)CP_T * (CP_T + L - 1);
+    const size_t img = img_bytes(L, Lp);
     size_t px = 0;  // levels 1..F-2 are staged (the last fused level is only written)
     for (int l = 1, T = CP_T / 2; l < F - 1; ++l, T >>= 1) px += (size_t)T * T;
-    return ((img + 15) & ~(size_t)15) + px * Lp * sizeof(int);
+    return img + px * Lp * sizeof(int);
 }
 
 cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArgs a, int B, cudaStream_t st)
 {
-    const size_t img = (size_t)CP_T * CP_T + (size_t)CP_T * (CP_T + a.L - 1);
-    a.img_smem = (int)((img + 15) & ~(size_t)15);
+    a.img_smem = (int)img_bytes(a.L, a.Lp);
     const size_t smem = costpyr_smem(a.L, a.Lp, a.F);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_costpyr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_costpyr_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        if (e == cudaSuccess)
+            e = cudaFuncSetAttribute(k_costpyr_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     dim3 grid((a.W[0] + CP_T - 1) / CP_T, (a.H[0] + CP_T - 1) / CP_T, B);
-    k_costpyr<<<grid, 256, smem, st>>>(left, right, a);
+    if (costpyr_fast_ok(a) && a.L % CH == 0)
+        k_costpyr_fast<false><<<grid, 256, smem, st>>>(left, right, a);
+    else if (costpyr_fast_ok(a))
+        k_costpyr_fast<true><<<grid, 256, smem, st>>>(left, right, a);
+    else
+        k_costpyr<<<grid, 256, smem, st>>>(left, right, a);
     note_launch();
     return cudaGetLastError();
 }

@@ -6,31 +6,47 @@
 //   log2 w_q = sx[tx] + sy[ty] - cr * (dist2(I_p, I_q) - ref)
 // with sx, sy = -log2(e)|p_down - q|^2/(2 sigma_s^2) split per axis (separable),
 // cr = log2(e)/(2 sigma_r^2), dist2 = the exact integer squared RGB distance
-// (VABSDIFF4 + IDP4A).  `ref` is any per-pixel constant (it cancels in the
-// ratio); it is the centre tap's dist2 when cr*that <= 4 (one pass, exponents
-// stay small so f32 rounding of the exponent is tiny), else the window minimum
-// (an extra integer pass).  Out-of-image taps get sx or sy = -inf (weight 0),
-// matching "taps outside the low-res image are skipped".  Rows are accumulated
-// separately and scaled by 2^sy at the end of the row.
+// (VABSDIFF4 + IDP4A).  The spatial terms depend only on the pixel's sub-position
+// (x mod s, y mod s) and the tap offset, so the host tabulates them once per call
+// (in double, rounded to f32): sxt[u][t] = sx and ryt[v][t] = 2^sy.  `ref` is any
+// per-pixel constant (it cancels in the ratio); it is the centre tap's dist2 when
+// cr*that <= 4 (one pass; exponents stay small so the f32 rounding of the exponent
+// is tiny), else the window minimum (an extra integer pass).  Out-of-image taps
+// get sx = -inf or a row factor of 0 (weight 0): "taps outside the low-res image
+// are skipped".  Rows are accumulated separately and scaled by 2^sy at the end.
 //
-// k_jbu_fast (any s): one thread = one full-res pixel; block = 32 x 8 pixels; the block's low-res
-// taps (guide sample + label) are staged once in shared memory as 8-byte records.
-// The reprojection [X Y Z W] = Q [u v D_p 1] follows in registers; xyz is written
-// through shared memory as coalesced 16-byte stores; one atomic per block counts
-// the points with D_p >= min_disp.
+// Two kernels, the same arithmetic in the same order (bit-identical results):
+//  * k_jbu_vec<R,S> (s = S in {2,4,8}): a thread owns P = min(S,4) horizontally
+//    adjacent pixels of one footprint row; they share the window, so each tap
+//    record is read from shared memory once for P pixels and pixel pairs run on the
+//    packed FP32x2 datapath (FADD2/FFMA2).  IDP4A yields the squared distance
+//    already as the float bit pattern 2^23 + (dist2 - ref) (accumulator input
+//    0x4B000000 + 2^22 - ref).  Per pixel-tap: VABSDIFF4, IDP4A, 1/2 FADD2,
+//    1/2 FFMA2, MUFU.EX2, 1/2 FFMA2, 1/2 FADD2 -- the EX2 (16/clk/SM) binds.
+//  * k_jbu_fast<R> (any s <= 16, or unaligned buffers): one thread per pixel.
+// k_jbu_vec threads own two rows of P pixels (block 32 x 4 threads), k_jbu_fast
+// one pixel (32 x 8); both cover a 32P x 8 pixel tile whose low-res taps (guide
+// sample + label) are staged once in shared memory as 8-byte records.  The reprojection
+// [X Y Z W] = Q [u v D_p 1] follows in registers (one reciprocal of W per pixel);
+// one atomic per block counts the points with D_p >= min_disp.
 #include <math.h>
+#include <stdlib.h>
+#include <string.h>
 
 #include "vsbp_internal.cuh"
 #include "vsbp_kernels.h"
 
 namespace vsbp {
 
-constexpr int JB_X = 32, JB_Y = 8, JB_RMAX = 8;
+constexpr int JB_X = 32, JB_Y = 8, JB_RMAX = 8, JB_SMAX = 16, JB_TMAX = 2 * JB_RMAX + 1;
 constexpr int JB_LW = JB_X + 2 * JB_RMAX + 1, JB_LH = JB_Y + 2 * JB_RMAX + 1;
 
 struct JbuFastArgs {
     int W, H, s;
-    float inv_s, cs, cr;
+    float cr;
+    int far_thr;                  // centre dist2 above which the window minimum is the reference
+    float sxt[JB_SMAX][JB_TMAX];  // [x mod s][tap column]: log2 of the x spatial weight
+    float ryt[JB_SMAX][JB_TMAX];  // [y mod s][tap row]: the y spatial weight 2^sy
     float q[16];
     float min_disp;
     int do_xyz;
@@ -43,25 +59,12 @@ __device__ __forceinline__ float ex2(float x)
     return y;
 }
 
-template <int R>
-__global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ disp_lo, const uint8_t *__restrict__ guide,
-                                                  float *__restrict__ disp_hi, float *__restrict__ xyz,
-                                                  unsigned long long *__restrict__ n_valid, JbuFastArgs a)
+// stage the block's low-res taps: {guide RGB at the footprint's centre sample, label as f32}
+__device__ __forceinline__ void stage_taps(uint2 *sT, const uint8_t *G, const int32_t *Dl, int lx0, int ly0, int lw,
+                                           int lh, int s, int Wh, const JbuFastArgs &a, int nthreads)
 {
-    __shared__ uint2 sT[JB_LW * JB_LH];
-    __shared__ __align__(16) float sX[JB_Y][JB_X * 3];
-    __shared__ unsigned warp_cnt[8];
-    const int b = blockIdx.z;
-    const int s = a.s;
-    const int Wh = a.W * s, Hh = a.H * s;
-    const int x0 = blockIdx.x * JB_X, y0 = blockIdx.y * JB_Y;
-    const int lx0 = x0 / s - R, ly0 = y0 / s - R;
-    const int lw = min(x0 + JB_X - 1, Wh - 1) / s + R - lx0 + 1;
-    const int lh = min(y0 + JB_Y - 1, Hh - 1) / s + R - ly0 + 1;
-    const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
-    const int32_t *Dl = disp_lo + (size_t)b * a.H * a.W;
     const int tid = threadIdx.y * JB_X + threadIdx.x;
-    for (int e = tid; e < lw * lh; e += JB_X * JB_Y) {
+    for (int e = tid; e < lw * lh; e += nthreads) {
         const int qy = ly0 + e / lw, qx = lx0 + e % lw;
         uint2 rec = make_uint2(0u, 0u);
         if (qx >= 0 && qy >= 0 && qx < a.W && qy < a.H) {
@@ -71,6 +74,65 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
         }
         sT[e] = rec;
     }
+}
+
+// n / d with one MUFU.RCP (rel. error ~2^-22; the tolerances are 1e-4 px / 1e-5 rel)
+__device__ __forceinline__ float fast_div(float n, float d)
+{
+    float r;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(d));
+    return n * r;
+}
+
+// a7 for one pixel: Eq.3 with Q (R-20), NaN below min_disp (R-21).  Row i of
+// Q [u v D 1]^T is evaluated as fma(q_i2, D, fma(q_i0, u, fma(q_i1, v, q_i3)))
+// in both kernels (the vector kernel does the same on pixel pairs).
+__device__ __forceinline__ bool reproject_px(const JbuFastArgs &a, float fu, float fv, float D, float *o)
+{
+    o[0] = o[1] = o[2] = __int_as_float(0x7fc00000);
+    if (!(D >= a.min_disp)) return false;
+    float h[4];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) h[i] = fmaf(a.q[4 * i + 2], D, fmaf(a.q[4 * i], fu, fmaf(a.q[4 * i + 1], fv, a.q[4 * i + 3])));
+    const float rW = fast_div(1.0f, h[3]);
+    o[0] = h[0] * rW;
+    o[1] = h[1] * rW;
+    o[2] = h[2] * rW;
+    return true;
+}
+
+__device__ __forceinline__ void block_count(unsigned *warp_cnt, int cnt, unsigned long long *n_valid, int b,
+                                            int nwarps)
+{
+    cnt = __reduce_add_sync(FULL, cnt);
+    if (threadIdx.x == 0) warp_cnt[threadIdx.y] = (unsigned)cnt;
+    __syncthreads();
+    if (threadIdx.x == 0 && threadIdx.y == 0) {
+        unsigned n = 0;
+        for (int w = 0; w < nwarps; ++w) n += warp_cnt[w];
+        if (n) atomicAdd(n_valid + b, (unsigned long long)n);
+    }
+}
+
+// ---------------------------------------------------------------- one pixel per thread
+template <int R>
+__global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ disp_lo, const uint8_t *__restrict__ guide,
+                                                  float *__restrict__ disp_hi, float *__restrict__ xyz,
+                                                  unsigned long long *__restrict__ n_valid,
+                                                  const __grid_constant__ JbuFastArgs a)
+{
+    constexpr int T = 2 * R + 1;
+    __shared__ uint2 sT[JB_LW * JB_LH];
+    __shared__ unsigned warp_cnt[JB_Y];
+    const int b = blockIdx.z;
+    const int s = a.s;
+    const int Wh = a.W * s, Hh = a.H * s;
+    const int x0 = blockIdx.x * JB_X, y0 = blockIdx.y * JB_Y;
+    const int lx0 = x0 / s - R, ly0 = y0 / s - R;
+    const int lw = min(x0 + JB_X - 1, Wh - 1) / s + R - lx0 + 1;
+    const int lh = min(y0 + JB_Y - 1, Hh - 1) / s + R - ly0 + 1;
+    const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
+    stage_taps(sT, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, s, Wh, a, JB_X * JB_Y);
     __syncthreads();
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     const bool inside = x < Wh && y < Hh;
@@ -79,106 +141,64 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
         const uint8_t *gp = G + ((size_t)y * Wh + x) * 3;
         const unsigned Ip = (unsigned)gp[0] | ((unsigned)gp[1] << 8) | ((unsigned)gp[2] << 16);
         const int cx = x / s, cy = y / s;
-        const float fx = (x + 0.5f) * a.inv_s - 0.5f - (float)cx;  // p_down - c, in (-0.5, 0.5)
-        const float fy = (y + 0.5f) * a.inv_s - 0.5f - (float)cy;
-        float sxl[2 * R + 1], syl[2 * R + 1];
+        const int u = x - cx * s, v = y - cy * s;
+        float sxl[T], rfl[T];
 #pragma unroll
-        for (int t = 0; t < 2 * R + 1; ++t) {
-            const float dx = fx + (float)(R - t), dy = fy + (float)(R - t);
+        for (int t = 0; t < T; ++t) {
             const int qx = cx - R + t, qy = cy - R + t;
-            sxl[t] = (qx >= 0 && qx < a.W) ? -a.cs * dx * dx : -INFINITY;
-            syl[t] = (qy >= 0 && qy < a.H) ? -a.cs * dy * dy : -INFINITY;
+            sxl[t] = (qx >= 0 && qx < a.W) ? a.sxt[u][t] : -INFINITY;
+            rfl[t] = (qy >= 0 && qy < a.H) ? a.ryt[v][t] : 0.f;
         }
         const int e0 = (cy - R - ly0) * lw + (cx - R - lx0);
-        const uint2 cen = sT[e0 + R * lw + R];
-        unsigned ad = __vabsdiffu4(Ip, cen.x);
+        const unsigned ad = __vabsdiffu4(Ip, sT[e0 + R * lw + R].x);
         int ref = (int)__dp4a(ad, ad, 0u);
-        if (a.cr * (float)ref > 4.0f) {
+        if (ref > a.far_thr) {
             // the centre is far in colour: reference the window minimum instead
 #pragma unroll
-            for (int ty = 0; ty < 2 * R + 1; ++ty) {
-                if (syl[ty] == -INFINITY) continue;
-#pragma unroll
-                for (int tx = 0; tx < 2 * R + 1; ++tx) {
-                    if (sxl[tx] == -INFINITY) continue;
+            for (int ty = 0; ty < T; ++ty) {
+                if (rfl[ty] == 0.f) continue;
+                for (int tx = 0; tx < T; ++tx) {
+                    const int qx = cx - R + tx;
+                    if (qx < 0 || qx >= a.W) continue;
                     const unsigned adq = __vabsdiffu4(Ip, sT[e0 + ty * lw + tx].x);
                     ref = min(ref, (int)__dp4a(adq, adq, 0u));
                 }
             }
         }
         // exact float of (dist2 - ref) via the 2^23 magic: |dist2 - ref| < 2^22
-        const int off = (1 << 22) - ref;
+        const unsigned acc = 0x4B000000u + (1u << 22) - (unsigned)ref;
         float num = 0.f, den = 0.f;
 #pragma unroll
-        for (int ty = 0; ty < 2 * R + 1; ++ty) {
+        for (int ty = 0; ty < T; ++ty) {
             float nr = 0.f, dr = 0.f;
 #pragma unroll
-            for (int tx = 0; tx < 2 * R + 1; ++tx) {
+            for (int tx = 0; tx < T; ++tx) {
                 const uint2 t = sT[e0 + ty * lw + tx];
                 const unsigned adq = __vabsdiffu4(Ip, t.x);
-                const int n = (int)__dp4a(adq, adq, 0u) + off;
-                const float f = __int_as_float(0x4B000000 | n) - 12582912.0f;  // = dist2 - ref
+                const float f = __uint_as_float(__dp4a(adq, adq, acc)) - 12582912.0f;  // = dist2 - ref
                 const float w = ex2(fmaf(-a.cr, f, sxl[tx]));
                 nr = fmaf(w, __uint_as_float(t.y), nr);
                 dr += w;
             }
-            const float rf = ex2(syl[ty]);
-            num = fmaf(rf, nr, num);
-            den = fmaf(rf, dr, den);
+            num = fmaf(rfl[ty], nr, num);
+            den = fmaf(rfl[ty], dr, den);
         }
-        Dp = (float)s * (num / den);
+        Dp = (float)s * fast_div(num, den);
         disp_hi[((size_t)b * Hh + y) * Wh + x] = Dp;
     }
     if (!a.do_xyz) return;
-    // ---- a7: reprojection of this pixel, Eq.3 with Q (R-20, R-21)
-    const bool valid = inside && Dp >= a.min_disp;
-    float o0 = __int_as_float(0x7fc00000), o1 = o0, o2 = o0;
-    if (valid) {
-        const float fu = (float)x, fv = (float)y;
-        const float X = fmaf(a.q[0], fu, fmaf(a.q[1], fv, fmaf(a.q[2], Dp, a.q[3])));
-        const float Y = fmaf(a.q[4], fu, fmaf(a.q[5], fv, fmaf(a.q[6], Dp, a.q[7])));
-        const float Z = fmaf(a.q[8], fu, fmaf(a.q[9], fv, fmaf(a.q[10], Dp, a.q[11])));
-        const float Wq = fmaf(a.q[12], fu, fmaf(a.q[13], fv, fmaf(a.q[14], Dp, a.q[15])));
-        o0 = X / Wq;
-        o1 = Y / Wq;
-        o2 = Z / Wq;
+    float o[3];
+    const bool valid = inside && reproject_px(a, (float)x, (float)y, Dp, o);
+    if (inside) {
+        float *dst = xyz + (((size_t)b * Hh + y) * Wh + x) * 3;
+        dst[0] = o[0];
+        dst[1] = o[1];
+        dst[2] = o[2];
     }
-    float *row = sX[threadIdx.y];
-    row[3 * threadIdx.x] = o0;
-    row[3 * threadIdx.x + 1] = o1;
-    row[3 * threadIdx.x + 2] = o2;
-    const unsigned m = __ballot_sync(FULL, valid);
-    if (threadIdx.x == 0) warp_cnt[threadIdx.y] = __popc(m);
-    __syncwarp();
-    // the warp's 32 pixels are contiguous: 96 floats = 24 float4 when aligned
-    if (y < Hh) {
-        const int nx = min(JB_X, Wh - x0);
-        float *dst = xyz + (((size_t)b * Hh + y) * Wh + x0) * 3;
-        if (nx == JB_X && ((reinterpret_cast<uintptr_t>(dst) & 15) == 0)) {
-            if (threadIdx.x < 24)
-                reinterpret_cast<float4 *>(dst)[threadIdx.x] = reinterpret_cast<const float4 *>(row)[threadIdx.x];
-        } else {
-            for (int k = threadIdx.x; k < 3 * nx; k += 32) dst[k] = row[k];
-        }
-    }
-    __syncthreads();
-    if (tid == 0) {
-        unsigned n = 0;
-#pragma unroll
-        for (int w = 0; w < JB_Y; ++w) n += warp_cnt[w];
-        if (n) atomicAdd(n_valid + b, (unsigned long long)n);
-    }
+    block_count(warp_cnt, valid ? 1 : 0, n_valid, b, JB_Y);
 }
 
 // ---------------------------------------------------------------- P pixels per thread
-// k_jbu_vec: same arithmetic as k_jbu_fast, bit for bit, for s % P == 0 (P = 2, 4).
-// A thread owns P horizontally adjacent full-res pixels of one footprint row: they
-// share the window centre c, so each tap record is read from shared memory once
-// for P pixels, the row factor 2^sy is shared, and pixel pairs run on the packed
-// FP32x2 datapath (FADD2/FFMA2).  The integer squared RGB distance comes out of
-// IDP4A already as the float bit pattern 2^23 + (dist2 - ref): the accumulator
-// input is 0x4B000000 + 2^22 - ref.  Per pixel-tap: VABSDIFF4, IDP4A, 1/2 FADD2,
-// 1/2 FFMA2, MUFU.EX2, 1/2 FFMA2, 1/2 FADD2 -- the EX2 (16/clk/SM) is the bound.
 typedef unsigned long long f2_t;  // two f32 in one 64-bit register pair
 
 __device__ __forceinline__ f2_t pk2(float a, float b)
@@ -202,7 +222,7 @@ __device__ __forceinline__ f2_t add2(f2_t a, f2_t b)
 }
 
 template <int P> struct GuideVec;
-template <> struct GuideVec<4> {  // 12 bytes, 4-byte aligned (x0 % 4 == 0)
+template <> struct GuideVec<4> {  // 12 bytes, 4-byte aligned (x % 4 == 0)
     static __device__ __forceinline__ void load(const uint8_t *g, unsigned I[4])
     {
         const unsigned *w = reinterpret_cast<const unsigned *>(g);
@@ -223,107 +243,104 @@ template <> struct GuideVec<2> {  // 6 bytes, 2-byte aligned
     }
 };
 
-template <int R, int P>
-__global__ void __launch_bounds__(256) k_jbu_vec(const int32_t *__restrict__ disp_lo, const uint8_t *__restrict__ guide,
-                                                 float *__restrict__ disp_hi, float *__restrict__ xyz,
-                                                 unsigned long long *__restrict__ n_valid, JbuFastArgs a)
+template <int R, int S, int NR>
+__global__ void __launch_bounds__(JB_X * JB_Y / NR) k_jbu_vec(const int32_t *__restrict__ disp_lo,
+                                                           const uint8_t *__restrict__ guide,
+                                                           float *__restrict__ disp_hi, float *__restrict__ xyz,
+                                                           unsigned long long *__restrict__ n_valid,
+                                                           const __grid_constant__ JbuFastArgs a)
 {
     constexpr int T = 2 * R + 1;
+    constexpr int P = S < 4 ? S : 4;  // pixels per thread along x
+    // NR rows per thread: rows 2t, 2t+1 of a tile are in one footprint row pair (S even)
+    constexpr int NT = JB_X * JB_Y / NR;
     __shared__ uint2 sT[JB_LW * JB_LH];
-    __shared__ unsigned warp_cnt[8];
+    __shared__ unsigned warp_cnt[NT / 32];
     const int b = blockIdx.z;
-    const int s = a.s;
-    const int Wh = a.W * s, Hh = a.H * s;
+    const int Wh = a.W * S, Hh = a.H * S;
     const int x0 = blockIdx.x * (JB_X * P), y0 = blockIdx.y * JB_Y;
-    const int lx0 = x0 / s - R, ly0 = y0 / s - R;
-    const int lw = min(x0 + JB_X * P - 1, Wh - 1) / s + R - lx0 + 1;
-    const int lh = min(y0 + JB_Y - 1, Hh - 1) / s + R - ly0 + 1;
+    const int lx0 = x0 / S - R, ly0 = y0 / S - R;
+    const int lw = min(x0 + JB_X * P - 1, Wh - 1) / S + R - lx0 + 1;
+    const int lh = min(y0 + JB_Y - 1, Hh - 1) / S + R - ly0 + 1;
     const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
-    const int32_t *Dl = disp_lo + (size_t)b * a.H * a.W;
-    const int tid = threadIdx.y * JB_X + threadIdx.x;
-    for (int e = tid; e < lw * lh; e += JB_X * JB_Y) {
-        const int qy = ly0 + e / lw, qx = lx0 + e % lw;
-        uint2 rec = make_uint2(0u, 0u);
-        if (qx >= 0 && qy >= 0 && qx < a.W && qy < a.H) {
-            const uint8_t *g = G + ((size_t)(s * qy + s / 2) * Wh + (size_t)(s * qx + s / 2)) * 3;
-            rec.x = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
-            rec.y = __float_as_uint((float)Dl[(size_t)qy * a.W + qx]);
-        }
-        sT[e] = rec;
-    }
+    stage_taps(sT, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, S, Wh, a, NT);
     __syncthreads();
-    const int x = x0 + P * threadIdx.x, y = y0 + threadIdx.y;
-    const bool inside = x < Wh && y < Hh;  // Wh % P == 0: all P pixels or none
-    float Dp[P];
+    const int x = x0 + P * threadIdx.x, yb = y0 + NR * threadIdx.y;
+    const bool inside = x < Wh && yb < Hh;  // Wh % P == 0, Hh % NR == 0: all pixels or none
+    float Dp[NR][P];
 #pragma unroll
-    for (int k = 0; k < P; ++k) Dp[k] = 0.f;
+    for (int r = 0; r < NR; ++r)
+#pragma unroll
+        for (int k = 0; k < P; ++k) Dp[r][k] = 0.f;
     if (inside) {
-        unsigned Ip[P];
-        GuideVec<P>::load(G + ((size_t)y * Wh + x) * 3, Ip);
-        const int cx = x / s, cy = y / s;
-        const float fy = (y + 0.5f) * a.inv_s - 0.5f - (float)cy;
-        float syl[T];
+        unsigned Ip[NR][P];
+#pragma unroll
+        for (int r = 0; r < NR; ++r) GuideVec<P>::load(G + ((size_t)(yb + r) * Wh + x) * 3, Ip[r]);
+        const int cx = x / S, cy = yb / S;
+        const int u0 = S == P ? 0 : x - cx * S;
+        const int v0 = yb - cy * S;
+        float rfl[NR][T];
         f2_t sx2[P / 2][T];
 #pragma unroll
         for (int t = 0; t < T; ++t) {
-            const float dy = fy + (float)(R - t);
             const int qy = cy - R + t, qx = cx - R + t;
-            syl[t] = (qy >= 0 && qy < a.H) ? -a.cs * dy * dy : -INFINITY;
-            const bool okx = qx >= 0 && qx < a.W;
+            const bool oky = qy >= 0 && qy < a.H, okx = qx >= 0 && qx < a.W;
 #pragma unroll
-            for (int j = 0; j < P / 2; ++j) {
-                const float fx0 = (x + 2 * j + 0.5f) * a.inv_s - 0.5f - (float)cx;
-                const float fx1 = (x + 2 * j + 1.5f) * a.inv_s - 0.5f - (float)cx;
-                const float d0 = fx0 + (float)(R - t), d1 = fx1 + (float)(R - t);
-                sx2[j][t] = pk2(okx ? -a.cs * d0 * d0 : -INFINITY, okx ? -a.cs * d1 * d1 : -INFINITY);
-            }
+            for (int r = 0; r < NR; ++r) rfl[r][t] = oky ? a.ryt[v0 + r][t] : 0.f;
+#pragma unroll
+            for (int j = 0; j < P / 2; ++j)
+                sx2[j][t] = okx ? pk2(a.sxt[u0 + 2 * j][t], a.sxt[u0 + 2 * j + 1][t]) : pk2(-INFINITY, -INFINITY);
         }
         const int e0 = (cy - R - ly0) * lw + (cx - R - lx0);
         const unsigned cen = sT[e0 + R * lw + R].x;
-        int ref[P];
+        int ref[NR][P];
         bool far = false;
 #pragma unroll
-        for (int k = 0; k < P; ++k) {
-            const unsigned ad = __vabsdiffu4(Ip[k], cen);
-            ref[k] = (int)__dp4a(ad, ad, 0u);
-            far = far || a.cr * (float)ref[k] > 4.0f;
-        }
-        if (far) {
-            // some centre is far in colour: reference that pixel's window minimum
-            float sxk[T];
-#pragma unroll
-            for (int t = 0; t < T; ++t) {
-                float u, v;
-                upk2(sx2[0][t], u, v);
-                sxk[t] = u;
-            }
+        for (int r = 0; r < NR; ++r)
 #pragma unroll
             for (int k = 0; k < P; ++k) {
-                const unsigned ad = __vabsdiffu4(Ip[k], cen);
-                if (!(a.cr * (float)__dp4a(ad, ad, 0u) > 4.0f)) continue;
-                for (int ty = 0; ty < T; ++ty) {
-                    if (syl[ty] == -INFINITY) continue;
-                    for (int tx = 0; tx < T; ++tx) {
-                        if (sxk[tx] == -INFINITY) continue;
-                        const unsigned adq = __vabsdiffu4(Ip[k], sT[e0 + ty * lw + tx].x);
-                        ref[k] = min(ref[k], (int)__dp4a(adq, adq, 0u));
+                const unsigned ad = __vabsdiffu4(Ip[r][k], cen);
+                ref[r][k] = (int)__dp4a(ad, ad, 0u);
+                far = far || ref[r][k] > a.far_thr;
+            }
+        if (far) {
+            // some centre is far in colour: that pixel references its window minimum
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+#pragma unroll
+                for (int k = 0; k < P; ++k) {
+                    if (ref[r][k] <= a.far_thr) continue;
+#pragma unroll
+                    for (int ty = 0; ty < T; ++ty) {
+                        if (rfl[r][ty] == 0.f) continue;
+                        for (int tx = 0; tx < T; ++tx) {
+                            const int qx = cx - R + tx;
+                            if (qx < 0 || qx >= a.W) continue;
+                            const unsigned adq = __vabsdiffu4(Ip[r][k], sT[e0 + ty * lw + tx].x);
+                            ref[r][k] = min(ref[r][k], (int)__dp4a(adq, adq, 0u));
+                        }
                     }
                 }
-            }
         }
-        unsigned acc[P];
+        unsigned acc[NR][P];
 #pragma unroll
-        for (int k = 0; k < P; ++k) acc[k] = 0x4B000000u + (1u << 22) - (unsigned)ref[k];
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int k = 0; k < P; ++k) acc[r][k] = 0x4B000000u + (1u << 22) - (unsigned)ref[r][k];
         const f2_t magic = pk2(-12582912.0f, -12582912.0f);
         const f2_t ncr = pk2(-a.cr, -a.cr);
-        f2_t num[P / 2], den[P / 2];
+        f2_t num[NR][P / 2], den[NR][P / 2];
 #pragma unroll
-        for (int j = 0; j < P / 2; ++j) num[j] = den[j] = 0ull;
+        for (int r = 0; r < NR; ++r)
+#pragma unroll
+            for (int j = 0; j < P / 2; ++j) num[r][j] = den[r][j] = 0ull;
 #pragma unroll
         for (int ty = 0; ty < T; ++ty) {
-            f2_t nr[P / 2], dr[P / 2];
+            f2_t nr[NR][P / 2], dr[NR][P / 2];
 #pragma unroll
-            for (int j = 0; j < P / 2; ++j) nr[j] = dr[j] = 0ull;
+            for (int r = 0; r < NR; ++r)
+#pragma unroll
+                for (int j = 0; j < P / 2; ++j) nr[r][j] = dr[r][j] = 0ull;
             const uint2 *row = sT + e0 + ty * lw;
 #pragma unroll
             for (int tx = 0; tx < T; ++tx) {
@@ -331,145 +348,182 @@ __global__ void __launch_bounds__(256) k_jbu_vec(const int32_t *__restrict__ dis
                 const float dq = __uint_as_float(tp.y);
                 const f2_t dd = pk2(dq, dq);
 #pragma unroll
+                for (int r = 0; r < NR; ++r)
+#pragma unroll
+                    for (int j = 0; j < P / 2; ++j) {
+                        const unsigned a0 = __vabsdiffu4(Ip[r][2 * j], tp.x), a1 = __vabsdiffu4(Ip[r][2 * j + 1], tp.x);
+                        const f2_t F = pk2(__uint_as_float(__dp4a(a0, a0, acc[r][2 * j])),
+                                           __uint_as_float(__dp4a(a1, a1, acc[r][2 * j + 1])));
+                        const f2_t ex = fma2(ncr, add2(F, magic), sx2[j][tx]);
+                        float e0f, e1f;
+                        upk2(ex, e0f, e1f);
+                        const f2_t w = pk2(ex2(e0f), ex2(e1f));
+                        nr[r][j] = fma2(w, dd, nr[r][j]);
+                        dr[r][j] = add2(w, dr[r][j]);
+                    }
+            }
+#pragma unroll
+            for (int r = 0; r < NR; ++r) {
+                const f2_t rf2 = pk2(rfl[r][ty], rfl[r][ty]);
+#pragma unroll
                 for (int j = 0; j < P / 2; ++j) {
-                    const unsigned a0 = __vabsdiffu4(Ip[2 * j], tp.x), a1 = __vabsdiffu4(Ip[2 * j + 1], tp.x);
-                    const f2_t F = pk2(__uint_as_float(__dp4a(a0, a0, acc[2 * j])),
-                                       __uint_as_float(__dp4a(a1, a1, acc[2 * j + 1])));
-                    const f2_t ex = fma2(ncr, add2(F, magic), sx2[j][tx]);
-                    float e0f, e1f;
-                    upk2(ex, e0f, e1f);
-                    const f2_t w = pk2(ex2(e0f), ex2(e1f));
-                    nr[j] = fma2(w, dd, nr[j]);
-                    dr[j] = add2(w, dr[j]);
+                    num[r][j] = fma2(rf2, nr[r][j], num[r][j]);
+                    den[r][j] = fma2(rf2, dr[r][j], den[r][j]);
                 }
             }
-            const float rf = ex2(syl[ty]);
-            const f2_t rf2 = pk2(rf, rf);
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
 #pragma unroll
             for (int j = 0; j < P / 2; ++j) {
-                num[j] = fma2(rf2, nr[j], num[j]);
-                den[j] = fma2(rf2, dr[j], den[j]);
+                float n0, n1, d0, d1;
+                upk2(num[r][j], n0, n1);
+                upk2(den[r][j], d0, d1);
+                Dp[r][2 * j] = (float)S * fast_div(n0, d0);
+                Dp[r][2 * j + 1] = (float)S * fast_div(n1, d1);
             }
+            float *dst = disp_hi + ((size_t)b * Hh + yb + r) * Wh + x;
+            if (P == 4)
+                *reinterpret_cast<float4 *>(dst) = make_float4(Dp[r][0], Dp[r][1], Dp[r][2], Dp[r][3]);
+            else
+                *reinterpret_cast<float2 *>(dst) = make_float2(Dp[r][0], Dp[r][1]);
         }
-#pragma unroll
-        for (int j = 0; j < P / 2; ++j) {
-            float n0, n1, d0, d1;
-            upk2(num[j], n0, n1);
-            upk2(den[j], d0, d1);
-            Dp[2 * j] = (float)s * (n0 / d0);
-            Dp[2 * j + 1] = (float)s * (n1 / d1);
-        }
-        float *dst = disp_hi + ((size_t)b * Hh + y) * Wh + x;
-        if (P == 4)
-            *reinterpret_cast<float4 *>(dst) = make_float4(Dp[0], Dp[1], Dp[2], Dp[3]);
-        else
-            *reinterpret_cast<float2 *>(dst) = make_float2(Dp[0], Dp[1]);
     }
     if (!a.do_xyz) return;
-    // ---- a7: reprojection, Eq.3 with Q (R-20, R-21); 3P contiguous floats per thread
-    float o[3 * P];
+    // ---- a7: 3P contiguous floats per thread and row, pixel pairs on FFMA2
     int cnt = 0;
+    f2_t q2[16];
 #pragma unroll
-    for (int k = 0; k < P; ++k) {
-        const bool valid = inside && Dp[k] >= a.min_disp;
-        float o0 = __int_as_float(0x7fc00000), o1 = o0, o2 = o0;
-        if (valid) {
-            const float fu = (float)(x + k), fv = (float)y, D = Dp[k];
-            const float X = fmaf(a.q[0], fu, fmaf(a.q[1], fv, fmaf(a.q[2], D, a.q[3])));
-            const float Y = fmaf(a.q[4], fu, fmaf(a.q[5], fv, fmaf(a.q[6], D, a.q[7])));
-            const float Z = fmaf(a.q[8], fu, fmaf(a.q[9], fv, fmaf(a.q[10], D, a.q[11])));
-            const float Wq = fmaf(a.q[12], fu, fmaf(a.q[13], fv, fmaf(a.q[14], D, a.q[15])));
-            o0 = X / Wq;
-            o1 = Y / Wq;
-            o2 = Z / Wq;
-            ++cnt;
-        }
-        o[3 * k] = o0;
-        o[3 * k + 1] = o1;
-        o[3 * k + 2] = o2;
-    }
-    if (inside) {
-        float *dst = xyz + (((size_t)b * Hh + y) * Wh + x) * 3;
-        if (P == 4) {
-            float4 *d4 = reinterpret_cast<float4 *>(dst);
-            d4[0] = make_float4(o[0], o[1], o[2], o[3]);
-            d4[1] = make_float4(o[4], o[5], o[6], o[7]);
-            d4[2] = make_float4(o[8], o[9], o[10], o[11]);
-        } else {
-            float2 *d2 = reinterpret_cast<float2 *>(dst);
-            d2[0] = make_float2(o[0], o[1]);
-            d2[1] = make_float2(o[2], o[3]);
-            d2[2] = make_float2(o[4], o[5]);
-        }
-    }
-    cnt = __reduce_add_sync(FULL, cnt);
-    if (threadIdx.x == 0) warp_cnt[threadIdx.y] = (unsigned)cnt;
-    __syncthreads();
-    if (tid == 0) {
-        unsigned n = 0;
+    for (int i = 0; i < 16; ++i) q2[i] = pk2(a.q[i], a.q[i]);
 #pragma unroll
-        for (int w = 0; w < JB_Y; ++w) n += warp_cnt[w];
-        if (n) atomicAdd(n_valid + b, (unsigned long long)n);
+    for (int r = 0; r < NR; ++r) {
+        const float fv = (float)(yb + r);
+        float o[3 * P];
+#pragma unroll
+        for (int j = 0; j < P / 2; ++j) {
+            const f2_t u2 = pk2((float)(x + 2 * j), (float)(x + 2 * j + 1)), v2 = pk2(fv, fv);
+            const f2_t D2 = pk2(Dp[r][2 * j], Dp[r][2 * j + 1]);
+            float h[4][2];
+#pragma unroll
+            for (int i = 0; i < 4; ++i) {
+                const f2_t hi = fma2(q2[4 * i + 2], D2, fma2(q2[4 * i], u2, fma2(q2[4 * i + 1], v2, q2[4 * i + 3])));
+                upk2(hi, h[i][0], h[i][1]);
+            }
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const int k = 2 * j + e;
+                const bool valid = inside && Dp[r][k] >= a.min_disp;
+                const float rW = fast_div(1.0f, h[3][e]);
+                const float nan = __int_as_float(0x7fc00000);
+                o[3 * k] = valid ? h[0][e] * rW : nan;
+                o[3 * k + 1] = valid ? h[1][e] * rW : nan;
+                o[3 * k + 2] = valid ? h[2][e] * rW : nan;
+                cnt += valid ? 1 : 0;
+            }
+        }
+        if (inside) {
+            float *dst = xyz + (((size_t)b * Hh + yb + r) * Wh + x) * 3;
+            if (P == 4) {
+                float4 *d4 = reinterpret_cast<float4 *>(dst);
+                d4[0] = make_float4(o[0], o[1], o[2], o[3]);
+                d4[1] = make_float4(o[4], o[5], o[6], o[7]);
+                d4[2] = make_float4(o[8], o[9], o[10], o[11]);
+            } else {
+                float2 *d2 = reinterpret_cast<float2 *>(dst);
+                d2[0] = make_float2(o[0], o[1]);
+                d2[1] = make_float2(o[2], o[3]);
+                d2[2] = make_float2(o[4], o[5]);
+            }
+        }
+    }
+    block_count(warp_cnt, cnt, n_valid, b, NT / 32);
+}
+
+// ---------------------------------------------------------------- launch
+template <int S, int NR>
+static void launch_vec(int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo, const uint8_t *guide,
+                       float *disp_hi, float *xyz, unsigned long long *n_valid, const JbuFastArgs &a)
+{
+    const dim3 block(JB_X, JB_Y / NR);
+    switch (radius) {
+    case 1: k_jbu_vec<1, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 2: k_jbu_vec<2, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 3: k_jbu_vec<3, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 4: k_jbu_vec<4, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 5: k_jbu_vec<5, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 6: k_jbu_vec<6, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 7: k_jbu_vec<7, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    default: k_jbu_vec<8, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     }
 }
 
-template <int P>
-static void launch_vec(int radius, dim3 grid, dim3 block, cudaStream_t st, const int32_t *disp_lo,
-                       const uint8_t *guide, float *disp_hi, float *xyz, unsigned long long *n_valid,
-                       const JbuFastArgs &a)
+template <int S>
+static void launch_vec_rows(int rows, int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo,
+                            const uint8_t *guide, float *disp_hi, float *xyz, unsigned long long *n_valid,
+                            const JbuFastArgs &a)
 {
-    switch (radius) {
-    case 1: k_jbu_vec<1, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 2: k_jbu_vec<2, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 3: k_jbu_vec<3, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 4: k_jbu_vec<4, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 5: k_jbu_vec<5, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 6: k_jbu_vec<6, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 7: k_jbu_vec<7, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    default: k_jbu_vec<8, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    }
+    if (rows == 1)
+        launch_vec<S, 1>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+    else
+        launch_vec<S, 2>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
 }
 
 cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
                             float sigma_s, float sigma_r, int radius, const float *Qf, float min_disp, float *xyz,
                             unsigned long long *n_valid, cudaStream_t st)
 {
+    if (s > JB_SMAX || radius > JB_RMAX) return cudaErrorInvalidValue;
     const double log2e = 1.4426950408889634;
+    const double cs = log2e / (2.0 * (double)sigma_s * sigma_s);
     JbuFastArgs a;
+    memset(&a, 0, sizeof a);
     a.W = W;
     a.H = H;
     a.s = s;
-    a.inv_s = (float)(1.0 / s);
-    a.cs = (float)(log2e / (2.0 * (double)sigma_s * sigma_s));
     a.cr = (float)(log2e / (2.0 * (double)sigma_r * sigma_r));
+    a.far_thr = (int)floor(4.0 / (double)a.cr);  // reference the minimum when cr * dist2 > ~4
+    // spatial tables (R-15): sub-position u of a footprint has p_down - c = (u + 0.5)/s - 0.5
+    for (int u = 0; u < s; ++u) {
+        const double f = (u + 0.5) / s - 0.5;
+        for (int t = 0; t <= 2 * radius; ++t) {
+            const double d = f + (double)(radius - t);
+            a.sxt[u][t] = (float)(-cs * d * d);
+            a.ryt[u][t] = (float)exp2(-cs * d * d);
+        }
+    }
     for (int i = 0; i < 16; ++i) a.q[i] = Qf ? Qf[i] : 0.f;
     a.min_disp = min_disp;
     a.do_xyz = xyz != nullptr;
     dim3 block(JB_X, JB_Y);
-    // the vector path needs P-aligned guide words and 4P-byte aligned outputs
+    // the vector kernel needs P-aligned guide words and 4P-byte aligned outputs
     const auto al = [](const void *p, uintptr_t m) { return ((uintptr_t)p & (m - 1)) == 0; };
-    int P = (s % 4 == 0) ? 4 : (s % 2 == 0) ? 2 : 1;
-    if (P == 4 && !(al(guide, 4) && al(disp_hi, 16) && al(xyz, 16))) P = (al(guide, 2) && al(disp_hi, 8) && al(xyz, 8)) ? 2 : 1;
-    if (P == 2 && !(al(guide, 2) && al(disp_hi, 8) && al(xyz, 8))) P = 1;
-    if (P > 1) {
+    const int P = s >= 4 ? 4 : 2;
+    const bool vec = (s == 2 || s == 4 || s == 8) && al(guide, P == 4 ? 4 : 2) && al(disp_hi, 4 * P) && al(xyz, 4 * P);
+    if (vec) {
+        // rows per thread of the vector kernel (tuning knob; both give identical results)
+        static const int rows = [] {
+            const char *e = getenv("VSBP_JBU_ROWS");
+            return (e && e[0] == '1') ? 1 : 2;
+        }();
         dim3 grid((W * s + JB_X * P - 1) / (JB_X * P), (H * s + JB_Y - 1) / JB_Y, B);
-        if (P == 4)
-            launch_vec<4>(radius, grid, block, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        if (s == 2)
+            launch_vec_rows<2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        else if (s == 4)
+            launch_vec_rows<4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else
-            launch_vec<2>(radius, grid, block, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
-        note_launch();
-        return cudaGetLastError();
-    }
-    dim3 grid((W * s + JB_X - 1) / JB_X, (H * s + JB_Y - 1) / JB_Y, B);
-    switch (radius) {
-    case 1: k_jbu_fast<1><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 2: k_jbu_fast<2><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 3: k_jbu_fast<3><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 4: k_jbu_fast<4><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 5: k_jbu_fast<5><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 6: k_jbu_fast<6><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 7: k_jbu_fast<7><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    default: k_jbu_fast<8><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+            launch_vec_rows<8>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+    } else {
+        dim3 grid((W * s + JB_X - 1) / JB_X, (H * s + JB_Y - 1) / JB_Y, B);
+        switch (radius) {
+        case 1: k_jbu_fast<1><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 2: k_jbu_fast<2><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 3: k_jbu_fast<3><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 4: k_jbu_fast<4><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 5: k_jbu_fast<5><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 6: k_jbu_fast<6><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        case 7: k_jbu_fast<7><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        default: k_jbu_fast<8><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+        }
     }
     note_launch();
     return cudaGetLastError();
