@@ -55,6 +55,8 @@ def lib():
         dbl = C.c_double
         L.oracle_quantize.argtypes = [f, f, f, p]
         L.oracle_prep.argtypes = [p, i, i, i, p]
+        L.oracle_undistort_map.argtypes = [i, i, p, p, p]
+        L.oracle_remap_rgb.argtypes = [p, i, i, p, p, p]
         L.oracle_cost_volume.argtypes = [p, p, i, i, i, C.c_int32, C.c_int32, p]
         L.oracle_pyramid_down.argtypes = [p, i, i, i, p]
         L.oracle_message.argtypes = [p, i, C.c_int32, C.c_int32, p]
@@ -115,6 +117,39 @@ def prep(rgb: np.ndarray, s: int) -> np.ndarray:
     out = np.zeros((H // s, W // s), np.uint8)
     _check(lib().oracle_prep(_ptr(rgb), W, H, s, _ptr(out)), "oracle_prep")
     return out
+
+
+def undistort_map(W: int, H: int, cam) -> tuple[np.ndarray, np.ndarray]:
+    """f1 (§2.1 radial-only undistortion, cvInitUndistortMap; R-26):
+    destination -> source map in 1/32 px, int32 [H][W] each.
+    cam = (f_u, f_v, c_u, c_v, k1, k2, k3)."""
+    c = np.ascontiguousarray(np.asarray(cam, np.float64).reshape(7))
+    mx = np.zeros((H, W), np.int32)
+    my = np.zeros((H, W), np.int32)
+    _check(lib().oracle_undistort_map(W, H, _ptr(c), _ptr(mx), _ptr(my)), "oracle_undistort_map")
+    return mx, my
+
+
+def remap_rgb(rgb: np.ndarray, map_x: np.ndarray, map_y: np.ndarray) -> np.ndarray:
+    """f1 (P:26 cvRemap; R-27): integer bilinear remap, zero outside."""
+    rgb = np.ascontiguousarray(rgb, np.uint8)
+    H, W, _ = rgb.shape
+    mx = np.ascontiguousarray(map_x, np.int32)
+    my = np.ascontiguousarray(map_y, np.int32)
+    if mx.shape != (H, W) or my.shape != (H, W):
+        raise ValueError("map must be [H][W]")
+    out = np.zeros_like(rgb)
+    _check(lib().oracle_remap_rgb(_ptr(rgb), W, H, _ptr(mx), _ptr(my), _ptr(out)), "oracle_remap_rgb")
+    return out
+
+
+def rectify_prep(rgb: np.ndarray, cam, s: int) -> tuple[np.ndarray, np.ndarray]:
+    """f1 + a0: undistort the RGB frame, then grey + s x s box mean.  Returns
+    (rectified RGB, grey low-res)."""
+    H, W, _ = rgb.shape
+    mx, my = undistort_map(W, H, cam)
+    rect = remap_rgb(rgb, mx, my)
+    return rect, prep(rect, s)
 
 
 def cost_volume(left: np.ndarray, right: np.ndarray, L: int, q: QParams) -> np.ndarray:

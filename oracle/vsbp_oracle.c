@@ -510,3 +510,80 @@ int oracle_disp_summary(const int32_t *disp, int W, int H, int64_t *label_sum, u
     *label_hash = hash;
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* F1  rectification: undistortion map + bilinear remap  (§2.1: "only     */
+/*     radial distortion and does not have any tangential distortion";         */
+/*     "rectify and undistort individual images ... cvInitUndistortMap() and   */
+/*     cvRemap()"; R-26, R-27)                          */
+/* ------------------------------------------------------------------------- */
+
+/* Destination -> source map ("maps are built destination->source"),
+ * cam = {f_u, f_v, c_u, c_v, k1, k2, k3}, new camera matrix = old (no extrinsic
+ * rectification for virtual pairs).  For destination pixel (u, v):
+ *   x = (u - c_u) / f_u,  y = (v - c_v) / f_v,  r2 = x*x + y*y
+ *   kr = 1 + k1*r2 + k2*r2*r2 + k3*r2*r2*r2          (radial only)
+ *   src_u = f_u*x*kr + c_u,  src_v = f_v*y*kr + c_v
+ * evaluated in double, left to right as written, then quantised to 1/32 px
+ * (R-26: the 5 fractional bits of OpenCV's remap tables):
+ *   map = floor(src * 32 + 0.5).                                              */
+int oracle_undistort_map(int W, int H, const double *cam, int32_t *map_x, int32_t *map_y)
+{
+    if (W < 1 || H < 1 || !cam || !map_x || !map_y) return OR_EINVAL;
+    const double fu = cam[0], fv = cam[1], cu = cam[2], cv = cam[3];
+    const double k1 = cam[4], k2 = cam[5], k3 = cam[6];
+    if (!(fu > 0.0) || !(fv > 0.0)) return OR_EINVAL;
+    for (int v = 0; v < H; ++v) {
+        for (int u = 0; u < W; ++u) {
+            double x = ((double)u - cu) / fu;
+            double y = ((double)v - cv) / fv;
+            double r2 = x * x + y * y;
+            double kr = 1.0 + k1 * r2 + k2 * r2 * r2 + k3 * r2 * r2 * r2;
+            double su = fu * x * kr + cu;
+            double sv = fv * y * kr + cv;
+            double qx = floor(su * 32.0 + 0.5), qy = floor(sv * 32.0 + 0.5);
+            if (!(fabs(qx) < 1073741824.0) || !(fabs(qy) < 1073741824.0)) return OR_EOVERFLOW;
+            map_x[(size_t)v * W + u] = (int32_t)qx;
+            map_y[(size_t)v * W + u] = (int32_t)qy;
+        }
+    }
+    return OR_OK;
+}
+
+/* floor(a / 32) for any int32 a */
+static int32_t floor_div32(int32_t a)
+{
+    return a >= 0 ? a / 32 : -((-(int64_t)a + 31) / 32);
+}
+
+/* Bilinear remap of an RGB image through a 1/32-px map (cvRemap, INTER_LINEAR,
+ * BORDER_CONSTANT 0; "out-of-bounds sources produce 0").  R-27: integer
+ * weights wx = {32 - ax, ax}, wy = {32 - ay, ay} (sum 1024), per channel
+ *   out = (sum_{i,j} wx_i * wy_j * I(ix+i, iy+j) + 512) >> 10
+ * with I = 0 outside the source image.                                        */
+int oracle_remap_rgb(const uint8_t *src, int W, int H, const int32_t *map_x, const int32_t *map_y,
+                     uint8_t *dst)
+{
+    if (!src || !dst || !map_x || !map_y || W < 1 || H < 1) return OR_EINVAL;
+    for (int v = 0; v < H; ++v) {
+        for (int u = 0; u < W; ++u) {
+            int32_t sx = map_x[(size_t)v * W + u], sy = map_y[(size_t)v * W + u];
+            int32_t ix = floor_div32(sx), iy = floor_div32(sy);
+            int32_t ax = sx - 32 * ix, ay = sy - 32 * iy;
+            int32_t wx[2] = {32 - ax, ax}, wy[2] = {32 - ay, ay};
+            for (int c = 0; c < 3; ++c) {
+                int64_t acc = 0;
+                for (int j = 0; j < 2; ++j) {
+                    for (int i = 0; i < 2; ++i) {
+                        int64_t px = (int64_t)ix + i, py = (int64_t)iy + j;
+                        int val = 0;
+                        if (px >= 0 && py >= 0 && px < W && py < H) val = src[3 * ((size_t)py * W + (size_t)px) + c];
+                        acc += (int64_t)wx[i] * wy[j] * val;
+                    }
+                }
+                dst[3 * ((size_t)v * W + u) + c] = (uint8_t)((acc + 512) >> 10);
+            }
+        }
+    }
+    return OR_OK;
+}

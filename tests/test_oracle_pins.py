@@ -370,3 +370,73 @@ def test_disp_summary_hash_known_value():
     d = np.array([[3, 4]], np.int32)
     s, _ = oracle.disp_summary(d)
     assert s == 7
+
+
+# ----------------------------------------------------------------------------- f1 rectification
+def test_undistort_map_golden(golden):
+    """Hand-worked radial maps (P:26 radial only; R-26)."""
+    for case in golden("undistort.json")["cases"]:
+        u, v = case["uv"]
+        mx, my = oracle.undistort_map(u + 3, v + 3, case["cam"])
+        assert [int(mx[v, u]), int(my[v, u])] == case["map"], case["note"]
+
+
+def test_undistort_zero_distortion_is_identity_and_principal_point_fixed():
+    mx, my = oracle.undistort_map(37, 23, (31.0, 29.0, 17.3, 9.6, 0.0, 0.0, 0.0))
+    vv, uu = np.mgrid[0:23, 0:37]
+    assert np.array_equal(mx, 32 * uu) and np.array_equal(my, 32 * vv)  # S:67 identity
+    for k in [(0.3, 0, 0), (-0.2, 0.05, 0.01), (0, 0, 1.0)]:
+        mx, my = oracle.undistort_map(41, 31, (40.0, 40.0, 20.0, 15.0) + k)
+        assert mx[15, 20] == 32 * 20 and my[15, 20] == 32 * 15  # principal point (S:67)
+
+
+def test_undistort_radial_symmetry():
+    """Radial model: mirror-symmetric about the principal point, the displacement
+    is along the ray from it, and |src - c| grows with k1 > 0 (barrel correction)."""
+    W = H = 41
+    mx, my = oracle.undistort_map(W, H, (30.0, 30.0, 20.0, 20.0, 0.2, 0.0, 0.0))
+    assert np.array_equal(mx - 640, -(mx[:, ::-1] - 640))
+    assert np.array_equal(my - 640, -(my[::-1, :] - 640))
+    vv, uu = np.mgrid[0:H, 0:W]
+    du, dv = uu - 20, vv - 20
+    r_dst = np.hypot(du, dv)
+    r_src = np.hypot(mx / 32 - 20, my / 32 - 20)
+    assert np.all(r_src >= r_dst - 1 / 32)
+    cross = (mx / 32 - 20) * dv - (my / 32 - 20) * du
+    assert np.max(np.abs(cross)) <= r_dst.max() / 32 + 1e-9
+
+
+def test_remap_identity_shift_and_ramp():
+    rng = np.random.default_rng(11)
+    img = rng.integers(0, 256, size=(9, 13, 3), dtype=np.uint8)
+    vv, uu = np.mgrid[0:9, 0:13].astype(np.int32)
+    assert np.array_equal(oracle.remap_rgb(img, 32 * uu, 32 * vv), img)  # S:72 identity
+    sh = oracle.remap_rgb(img, 32 * (uu + 1), 32 * vv)                     # S:73 integer shift
+    assert np.array_equal(sh[:, :-1], img[:, 1:]) and not sh[:, -1].any()
+    ramp = np.broadcast_to((2 * np.arange(13, dtype=np.uint8))[None, :, None], (9, 13, 3)).copy()
+    half = oracle.remap_rgb(ramp, 32 * uu + 16, 32 * vv)                   # S:74 half-pixel ramp
+    assert np.array_equal(half[:, :-1, 0], (2 * uu + 1)[:, :-1])
+    assert np.array_equal(half[:, -1, 0], (ramp[:, -1, 0].astype(int) + 1) // 2)  # right tap is outside (0)
+
+
+def test_remap_is_exact_on_affine_images():
+    """Bilinear interpolation reproduces an affine image exactly, so with the
+    integer weights the output is the affine value at the 1/32-px source point
+    rounded half up (R-27)."""
+    rng = np.random.default_rng(12)
+    H, W = 20, 30
+    a, b, c = 3, 5, 7  # I = 3u + 5v + 7 <= 3*29 + 5*19 + 7 = 189
+    vv, uu = np.mgrid[0:H, 0:W]
+    img = np.repeat((a * uu + b * vv + c).astype(np.uint8)[..., None], 3, axis=2)
+    mx = rng.integers(0, 32 * (W - 1), size=(H, W)).astype(np.int32)
+    my = rng.integers(0, 32 * (H - 1), size=(H, W)).astype(np.int32)
+    out = oracle.remap_rgb(img, mx, my)[..., 1].astype(np.int64)
+    num = a * mx.astype(np.int64) + b * my.astype(np.int64) + 32 * c   # 32 * exact value
+    assert np.array_equal(out, (num + 16) // 32)
+
+
+def test_rectify_prep_without_distortion_is_prep():
+    rgb = synthgen.value_noise_rgb(3, 64, 40)
+    rect, grey = oracle.rectify_prep(rgb, (50.0, 50.0, 31.5, 19.5, 0.0, 0.0, 0.0), 4)
+    assert np.array_equal(rect, rgb)
+    assert np.array_equal(grey, oracle.prep(rgb, 4))
