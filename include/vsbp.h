@@ -165,6 +165,24 @@ int prep_downsample_batch(int n, const uint8_t *rgb_hi, int W_hi, int H_hi, int 
 int prep_downsample(const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *gray_lo, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * rectify_prep_batch -- row f1 fused with a0 (§2.1: radial-only
+ * undistortion, "cvInitUndistortMap() and cvRemap()"; R-26, R-27):
+ *   rgb_raw  : u8 [n][H_hi][W_hi][3] distorted frames (device)
+ *   cam      : HOST pointer, double[7] = {f_u, f_v, c_u, c_v, k1, k2, k3} (pixels;
+ *              new camera matrix = old, no tangential terms); copied at call time
+ *   gray_lo  : u8 [n][H_hi/s][W_hi/s]: grey + s x s box mean (as prep_downsample)
+ *              of the undistorted frame
+ *   rgb_rect : u8 [n][H_hi][W_hi][3] undistorted frames, or NULL (not written)
+ * Destination pixel (u,v) samples the source at the radial map of R-26 quantised
+ * to 1/32 px; channels are interpolated with integer bilinear weights (R-27),
+ * taps outside the frame read 0.  s in 1..8; W_hi, H_hi multiples of s (else
+ * VSBP_EDIM); f_u, f_v <= 0 -> VSBP_EINVAL; a map that can leave |coordinate| <
+ * 2^24 px (R-26 bound) -> VSBP_EOVERFLOW.
+ * ------------------------------------------------------------------------- */
+int rectify_prep_batch(int n, const uint8_t *rgb_raw, int W_hi, int H_hi, const double *cam, int s,
+                       uint8_t *gray_lo, uint8_t *rgb_rect, void *stream);
+
+/* ---------------------------------------------------------------------------
  * pair_summary_batch -- a8: for B pairs write summary[b] =
  *   {n_valid[b], sum of disp_lo[b], label hash of disp_lo[b], first_pair_id + b}.
  *   disp_lo : int32 [B][H][W]; n_valid : device uint64 [B]; summary : device [B].

@@ -281,14 +281,20 @@ def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.nda
 
 
 def pipeline_pair(left_rgb, right_rgb, s, L, levels, iters, Q, lam=0.07, data_trunc=15.0,
-                  disc_trunc=1.7, sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0):
-    """a0-a8 for one pair, the oracle's way (used by bench.py's cpu_baseline)."""
+                  disc_trunc=1.7, sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, camera=None):
+    """a0-a8 for one pair, the oracle's way (used by bench.py's cpu_baseline);
+    with a camera the frames are undistorted first (row f1) and the rectified left
+    frame is the JBU guide."""
     if sigma_s is None:
         sigma_s = 15.0 / s
     if radius is None:
         radius = -(-5 // s)
-    gl = prep(left_rgb, s)
-    gr = prep(right_rgb, s)
+    if camera is not None:
+        left_rgb, gl = rectify_prep(left_rgb, camera, s)
+        _, gr = rectify_prep(right_rgb, camera, s)
+    else:
+        gl = prep(left_rgb, s)
+        gr = prep(right_rgb, s)
     disp = bp_disparity(gl, gr, L, levels, iters, lam, data_trunc, disc_trunc)
     hi = jbu(disp, left_rgb, s, sigma_s, sigma_r, radius)
     xyz, n = reproject(hi, Q, min_disp)

@@ -533,6 +533,16 @@ int oracle_undistort_map(int W, int H, const double *cam, int32_t *map_x, int32_
     const double fu = cam[0], fv = cam[1], cu = cam[2], cv = cam[3];
     const double k1 = cam[4], k2 = cam[5], k3 = cam[6];
     if (!(fu > 0.0) || !(fv > 0.0)) return OR_EINVAL;
+    /* domain (R-26): |source coordinate| < 2^24 px everywhere, by the bound
+     * |src| <= f*max|x|*(1 + |k1| r2m + |k2| r2m^2 + |k3| r2m^3) + |c| with the
+     * corner maxima max|x|, max|y|, r2m = max|x|^2 + max|y|^2 */
+    {
+        double xm = fmax(fabs((0.0 - cu) / fu), fabs(((double)(W - 1) - cu) / fu));
+        double ym = fmax(fabs((0.0 - cv) / fv), fabs(((double)(H - 1) - cv) / fv));
+        double r2m = xm * xm + ym * ym;
+        double K = 1.0 + fabs(k1) * r2m + fabs(k2) * r2m * r2m + fabs(k3) * r2m * r2m * r2m;
+        if (!(fu * xm * K + fabs(cu) < 16777216.0) || !(fv * ym * K + fabs(cv) < 16777216.0)) return OR_EOVERFLOW;
+    }
     for (int v = 0; v < H; ++v) {
         for (int u = 0; u < W; ++u) {
             double x = ((double)u - cu) / fu;
@@ -542,7 +552,6 @@ int oracle_undistort_map(int W, int H, const double *cam, int32_t *map_x, int32_
             double su = fu * x * kr + cu;
             double sv = fv * y * kr + cv;
             double qx = floor(su * 32.0 + 0.5), qy = floor(sv * 32.0 + 0.5);
-            if (!(fabs(qx) < 1073741824.0) || !(fabs(qy) < 1073741824.0)) return OR_EOVERFLOW;
             map_x[(size_t)v * W + u] = (int32_t)qx;
             map_y[(size_t)v * W + u] = (int32_t)qy;
         }

@@ -67,6 +67,8 @@ _EXPORTS = {
     "prep_downsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                         C.c_void_p]),
     "prep_downsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "rectify_prep_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
+                                     C.c_void_p, C.c_void_p]),
     "pair_summary_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
                                      C.c_void_p, C.c_void_p]),
     "bp_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
@@ -226,6 +228,30 @@ def jbu_upsample(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_s
     return out[0] if squeeze else out
 
 
+def rectify_prep(rgb_raw: torch.Tensor, cam, s: int, gray: torch.Tensor | None = None,
+                 rect: torch.Tensor | bool | None = None, stream=None):
+    """Row f1 + a0: undistort (radial k1..k3) and grey/box-downsample n frames.
+    rgb_raw uint8 [n,H,W,3] (or [H,W,3]); cam = (f_u, f_v, c_u, c_v, k1, k2, k3).
+    rect=True allocates the rectified RGB output (else pass a tensor, or None to
+    skip it).  Returns (gray [n,H/s,W/s], rect or None)."""
+    squeeze = rgb_raw.dim() == 3
+    if squeeze:
+        rgb_raw = rgb_raw.unsqueeze(0)
+    n, H, W, _ = rgb_raw.shape
+    if gray is None:
+        gray = torch.empty((n, H // s, W // s), dtype=torch.uint8, device=rgb_raw.device)
+    if rect is True:
+        rect = torch.empty_like(rgb_raw)
+    camd = (C.c_double * 7)(*[float(v) for v in cam])
+    _check(lib().rectify_prep_batch(n, _dev(rgb_raw, torch.uint8, "rgb_raw"), W, H, camd, s,
+                                    _dev(gray, torch.uint8, "gray_lo"),
+                                    _dev(rect, torch.uint8, "rgb_rect") if rect is not None else None,
+                                    _stream(stream)), "rectify_prep_batch")
+    if squeeze:
+        return gray[0], (rect[0] if rect is not None else None)
+    return gray, rect
+
+
 def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.ndarray:
     """Eq.3 as a 4x4 reprojection matrix with z = f B/(d du) (R-20)."""
     return np.array([[1.0, 0.0, 0.0, -u0],
@@ -303,7 +329,8 @@ class StereoPipeline:
     reprojection, per-pair summary.  Buffers are allocated once."""
 
     def __init__(self, W_hi, H_hi, s, ndisp, levels, iters, batch, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
-                 sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0):
+                 sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0,
+                 camera=None):
         self.W_hi, self.H_hi, self.s, self.B = W_hi, H_hi, s, batch
         self.W, self.H = W_hi // s, H_hi // s
         self.sigma_s = 15.0 / s if sigma_s is None else sigma_s  # R-16
@@ -320,15 +347,26 @@ class StereoPipeline:
         self.xyz = torch.empty((batch, H_hi, W_hi, 3), dtype=torch.float32, device=dev)
         self.n_valid = torch.zeros(batch, dtype=torch.int64, device=dev)
         self.summary = torch.empty((batch, 8), dtype=torch.int64, device=dev)
+        # row f1: with a camera (f_u, f_v, c_u, c_v, k1, k2, k3) the raw frames are
+        # undistorted first (fused with a0); the rectified left frame is the JBU guide
+        self.camera = camera
+        self.rect = (torch.empty((batch, H_hi, W_hi, 3), dtype=torch.uint8, device=dev)
+                     if camera is not None else None)
 
     def run(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, first_pair_id: int = 0, stream=None):
         """left_rgb, right_rgb: uint8 [B,H_hi,W_hi,3] on the device.  Returns the
         per-pair summary tensor (device); disp / disp_hi / xyz stay in the object."""
         B = left_rgb.shape[0]
-        prep_downsample(left_rgb, self.s, out=self.gray[0, :B], stream=stream)
-        prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
+        if self.camera is not None:
+            rectify_prep(left_rgb, self.camera, self.s, gray=self.gray[0, :B], rect=self.rect[:B], stream=stream)
+            rectify_prep(right_rgb, self.camera, self.s, gray=self.gray[1, :B], stream=stream)
+            guide = self.rect[:B]
+        else:
+            prep_downsample(left_rgb, self.s, out=self.gray[0, :B], stream=stream)
+            prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
+            guide = left_rgb
         self.bp.disparity(self.gray[0, :B], self.gray[1, :B], out=self.disp[:B], stream=stream)
-        jbu_reproject(self.disp[:B], left_rgb, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
+        jbu_reproject(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
                       self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
                       stream=stream)
         return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=self.summary[:B], stream=stream)

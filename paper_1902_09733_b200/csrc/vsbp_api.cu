@@ -539,6 +539,20 @@ int prep_downsample(const uint8_t *rgb_hi, int W_hi, int H_hi, int s, uint8_t *g
     return prep_downsample_batch(1, rgb_hi, W_hi, H_hi, s, gray_lo, stream);
 }
 
+int rectify_prep_batch(int n, const uint8_t *rgb_raw, int W_hi, int H_hi, const double *cam, int s,
+                       uint8_t *gray_lo, uint8_t *rgb_rect, void *stream)
+{
+    if (n < 1 || !rgb_raw || !gray_lo || !cam || W_hi < 1 || H_hi < 1 || s < 1 || s > 8) return VSBP_EINVAL;
+    if (!(cam[0] > 0.0) || !(cam[1] > 0.0)) return VSBP_EINVAL;
+    for (int i = 0; i < 7; ++i)
+        if (!std::isfinite(cam[i])) return VSBP_EINVAL;
+    if (W_hi % s != 0 || H_hi % s != 0) return VSBP_EDIM;
+    if ((long long)W_hi * H_hi > (1ll << 28)) return VSBP_EINVAL;
+    if (!vsbp::rectify_domain_ok(W_hi, H_hi, cam)) return VSBP_EOVERFLOW;
+    CK(vsbp::launch_rectify_prep(n, rgb_raw, W_hi, H_hi, cam, s, gray_lo, rgb_rect, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
 int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsigned long long *n_valid,
                        uint64_t first_pair_id, vsbp_summary *summary, void *stream)
 {

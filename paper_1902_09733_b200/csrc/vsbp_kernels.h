@@ -63,3 +63,10 @@ cudaError_t launch_summary(int B, const int32_t *disp, int W, int H, const unsig
                            uint64_t first_pair_id, void *summary, cudaStream_t st);
 
 }  // namespace vsbp
+
+namespace vsbp {
+// row f1 (rectify.cu): radial undistortion + bilinear remap fused with a0
+bool rectify_domain_ok(int W, int H, const double *cam);
+cudaError_t launch_rectify_prep(int n, const uint8_t *raw, int W, int H, const double *cam, int s, uint8_t *gray,
+                                uint8_t *rect, cudaStream_t st);
+}  // namespace vsbp

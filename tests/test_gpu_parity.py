@@ -303,3 +303,78 @@ def test_jbu_reproject_ragged(W, H, s, r):
     if valid.any():
         err = np.linalg.norm(xyz_g[valid] - xyz_o[valid], axis=1) / np.linalg.norm(xyz_o[valid], axis=1)
         assert err.max() <= 1e-5
+
+
+# ----------------------------------------------------------------------------- f1
+GOPRO_CAM = (1400.0, 1400.0, 1351.5, 759.5, -0.25, 0.08, -0.01)  # wide-angle barrel
+
+
+@pytest.mark.parametrize("W,H,s,cam", [
+    (64, 40, 4, (50.0, 50.0, 31.5, 19.5, 0.0, 0.0, 0.0)),
+    (64, 40, 4, (40.0, 45.0, 30.0, 21.0, 0.3, 0.0, 0.0)),
+    (66, 39, 3, (30.0, 30.0, 33.7, 18.2, -0.2, 0.04, 0.0)),
+    (34, 18, 2, (20.0, 22.0, 16.5, 8.5, 0.1, -0.05, 0.02)),
+    (23, 17, 1, (15.0, 15.0, 11.0, 8.0, -0.3, 0.1, -0.02)),
+    (96, 48, 8, (60.0, 60.0, 47.5, 23.5, 0.05, 0.0, 0.01)),
+    (40, 24, 4, (10.0, 10.0, 19.5, 11.5, 2.0, 0.0, 0.0)),   # strong: many sources outside the frame
+])
+def test_rectify_prep_bit_exact(W, H, s, cam):
+    rng = np.random.default_rng(W * H + s)
+    frames = [synthgen.value_noise_rgb(10 + i, W, H) for i in range(3)]
+    frames[2] = rng.integers(0, 256, size=(H, W, 3), dtype=np.uint8)
+    raw = to_dev(np.stack(frames))
+    gray, rect = P.rectify_prep(raw, cam, s, rect=True)
+    for i, f in enumerate(frames):
+        rect_o, gray_o = oracle.rectify_prep(f, cam, s)
+        assert np.array_equal(rect[i].cpu().numpy(), rect_o), f"rectified frame {i}"
+        assert np.array_equal(gray[i].cpu().numpy(), gray_o), f"grey frame {i}"
+
+
+def test_rectify_prep_full_frame_and_unaligned():
+    left, right, _ = synthgen.stereo_pair_rgb(5)
+    raw = to_dev(np.stack([left, right]))
+    gray, rect = P.rectify_prep(raw, GOPRO_CAM, 4, rect=True)
+    for i, f in enumerate([left, right]):
+        rect_o, gray_o = oracle.rectify_prep(f, GOPRO_CAM, 4)
+        assert np.array_equal(rect[i].cpu().numpy(), rect_o)
+        assert np.array_equal(gray[i].cpu().numpy(), gray_o)
+    # a frame that does not start on an 8-byte boundary takes the byte path: same result
+    small = synthgen.value_noise_rgb(9, 64, 40)
+    buf = torch.zeros(64 * 40 * 3 + 1, dtype=torch.uint8, device=dev())
+    buf[1:] = to_dev(small).reshape(-1)
+    g2, r2 = P.rectify_prep(buf[1:].view(40, 64, 3), (40.0, 45.0, 30.0, 21.0, 0.3, 0.0, 0.0), 4, rect=True)
+    rect_o, gray_o = oracle.rectify_prep(small, (40.0, 45.0, 30.0, 21.0, 0.3, 0.0, 0.0), 4)
+    assert np.array_equal(r2.cpu().numpy(), rect_o) and np.array_equal(g2.cpu().numpy(), gray_o)
+
+
+def test_rectify_prep_rejects():
+    raw = torch.zeros((1, 40, 64, 3), dtype=torch.uint8, device=dev())
+    with pytest.raises(P.VsbpError) as e:
+        P.rectify_prep(raw, (0.0, 50.0, 31.5, 19.5, 0, 0, 0), 4)
+    assert e.value.code == -1
+    with pytest.raises(P.VsbpError) as e:
+        P.rectify_prep(raw, (50.0, 50.0, 31.5, 19.5, 0, 0, 0), 9)
+    assert e.value.code == -1
+    with pytest.raises(P.VsbpError) as e:
+        P.rectify_prep(raw, (50.0, 50.0, 31.5, 19.5, 0, 0, 0), 3)
+    assert e.value.code == -2
+    cam = (50.0, 50.0, 31.5, 19.5, 1e12, 0, 0)
+    with pytest.raises(oracle.OracleError):
+        oracle.undistort_map(64, 40, cam)
+    with pytest.raises(P.VsbpError) as e:
+        P.rectify_prep(raw, cam, 4)
+    assert e.value.code == -3
+
+
+def test_pipeline_with_rectification_end_to_end():
+    """f1 + a0-a8: undistorted frames through the whole path, against the oracle."""
+    left, right, _ = synthgen.stereo_pair_rgb(6)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    pipe = P.StereoPipeline(2704, 1520, 4, 64, 5, 5, batch=1, Q=Q, device=dev(), camera=GOPRO_CAM)
+    summ = pipe.run(to_dev(left[None]), to_dev(right[None])).cpu().numpy()
+    disp_o, hi_o, xyz_o, n_o = oracle.pipeline_pair(left, right, 4, 64, 5, 5, Q, camera=GOPRO_CAM)
+    assert np.array_equal(pipe.disp[0].cpu().numpy(), disp_o)
+    assert np.max(np.abs(pipe.disp_hi[0].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
+    amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
+    assert abs(int(summ[0, 0]) - n_o) <= amb

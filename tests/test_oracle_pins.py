@@ -440,3 +440,12 @@ def test_rectify_prep_without_distortion_is_prep():
     rect, grey = oracle.rectify_prep(rgb, (50.0, 50.0, 31.5, 19.5, 0.0, 0.0, 0.0), 4)
     assert np.array_equal(rect, rgb)
     assert np.array_equal(grey, oracle.prep(rgb, 4))
+
+
+def test_undistort_domain_rejects_runaway_maps():
+    """R-26 domain: a map whose bound leaves |coordinate| < 2^24 px is rejected."""
+    with pytest.raises(oracle.OracleError) as e:
+        oracle.undistort_map(64, 40, (50.0, 50.0, 31.5, 19.5, 1e12, 0.0, 0.0))
+    assert e.value.code == -3
+    with pytest.raises(oracle.OracleError):
+        oracle.undistort_map(64, 40, (0.0, 50.0, 31.5, 19.5, 0.0, 0.0, 0.0))
