@@ -57,6 +57,10 @@ def lib():
         L.oracle_prep.argtypes = [p, i, i, i, p]
         L.oracle_undistort_map.argtypes = [i, i, p, p, p]
         L.oracle_remap_rgb.argtypes = [p, i, i, p, p, p]
+        L.oracle_harris_response.argtypes = [p, i, i, p]
+        L.oracle_harris_grid.argtypes = [p, i, i, i, i, i, C.c_int64, p, p, p]
+        L.oracle_zssd.argtypes = [p, p, i, i, i, i, i, i, i, p]
+        L.oracle_zssd_match.argtypes = [p, p, i, i, p, i, i, i, C.c_int64, p, p]
         L.oracle_cost_volume.argtypes = [p, p, i, i, i, C.c_int32, C.c_int32, p]
         L.oracle_pyramid_down.argtypes = [p, i, i, i, p]
         L.oracle_message.argtypes = [p, i, C.c_int32, C.c_int32, p]
@@ -150,6 +154,54 @@ def rectify_prep(rgb: np.ndarray, cam, s: int) -> tuple[np.ndarray, np.ndarray]:
     mx, my = undistort_map(W, H, cam)
     rect = remap_rgb(rgb, mx, my)
     return rect, prep(rect, s)
+
+
+def harris_response(img: np.ndarray) -> np.ndarray:
+    """f3 (Eq.4-5; R-28): 25 * Harris response, int64 [H][W]; INT64_MIN
+    outside 3 <= x <= W-4, 3 <= y <= H-4."""
+    img = np.ascontiguousarray(img, np.uint8)
+    H, W = img.shape
+    out = np.zeros((H, W), np.int64)
+    _check(lib().oracle_harris_response(_ptr(img), W, H, _ptr(out)), "oracle_harris_response")
+    return out
+
+
+def harris_grid(R25: np.ndarray, gc: int = 30, gr: int = 30, K: int = 4, thr: int = 1):
+    """f3 (P:84 30x30 grid; R-29): per-cell top-K strict local maxima.  Returns
+    (xy int32 [gr*gc*K][2], resp int64 [gr*gc*K], count int32 [gr*gc])."""
+    R = np.ascontiguousarray(R25, np.int64)
+    H, W = R.shape
+    xy = np.zeros((gr * gc * K, 2), np.int32)
+    resp = np.zeros(gr * gc * K, np.int64)
+    cnt = np.zeros(gr * gc, np.int32)
+    _check(lib().oracle_harris_grid(_ptr(R), W, H, gc, gr, K, int(thr), _ptr(xy), _ptr(resp), _ptr(cnt)),
+           "oracle_harris_grid")
+    return xy, resp, cnt
+
+
+def zssd(img1, img2, x1, y1, x2, y2, r) -> int:
+    """f3 (R-30): n * ZSSD of the n = (2r+1)^2 patches, exact integer."""
+    a = np.ascontiguousarray(img1, np.uint8)
+    b = np.ascontiguousarray(img2, np.uint8)
+    H, W = a.shape
+    out = np.zeros(1, np.int64)
+    _check(lib().oracle_zssd(_ptr(a), _ptr(b), W, H, x1, y1, x2, y2, r, _ptr(out)), "oracle_zssd")
+    return int(out[0])
+
+
+def zssd_match(img1, img2, xy: np.ndarray, r: int = 5, sr: int = 16, max_cost: int = 2 ** 62):
+    """f3 (R-31): best ZSSD match of every corner (slots with x < 0 are
+    skipped).  Returns (match int32 [n][2] or -1, cost int64 [n] or -1)."""
+    a = np.ascontiguousarray(img1, np.uint8)
+    b = np.ascontiguousarray(img2, np.uint8)
+    H, W = a.shape
+    xy = np.ascontiguousarray(xy, np.int32).reshape(-1, 2)
+    n = xy.shape[0]
+    m = np.zeros((n, 2), np.int32)
+    c = np.zeros(n, np.int64)
+    _check(lib().oracle_zssd_match(_ptr(a), _ptr(b), W, H, _ptr(xy), n, r, sr, int(max_cost), _ptr(m), _ptr(c)),
+           "oracle_zssd_match")
+    return m, c
 
 
 def cost_volume(left: np.ndarray, right: np.ndarray, L: int, q: QParams) -> np.ndarray:

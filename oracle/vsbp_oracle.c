@@ -596,3 +596,169 @@ int oracle_remap_rgb(const uint8_t *src, int W, int H, const int32_t *map_x, con
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* F3  Harris corners on a grid + ZSSD matching  (§2.3 Eq.4-5; P:84    */
+/*     "divide the imaging plane to a 30x30 grid and calculate Harris corners  */
+/*     inside each grid individually"; R-28..R-31)    */
+/* ------------------------------------------------------------------------- */
+
+/* R-28: Harris response scaled by 25 (k = 0.04 = 1/25), exact in int64.
+ *   A = I(x+1,y) - I(x-1,y),  B = I(x,y+1) - I(x,y-1)          (central differences)
+ *   Sxx = sum w*A*A, Sxy = sum w*A*B, Syy = sum w*B*B over the 5x5 window with the
+ *   binomial weights w(i,j) = b(i) b(j), b = {1,4,6,4,1}     (Eq.4's Gaussian w)
+ *   R25 = 25*(Sxx*Syy - Sxy*Sxy) - (Sxx + Syy)^2 = 25 * (det M - k tr^2 M)  (Eq.5)
+ * R25 is defined for 3 <= x <= W-4, 3 <= y <= H-4 and set to INT64_MIN elsewhere. */
+int oracle_harris_response(const uint8_t *img, int W, int H, int64_t *R25)
+{
+    static const int b[5] = {1, 4, 6, 4, 1};
+    if (!img || !R25 || W < 1 || H < 1) return OR_EINVAL;
+    for (int y = 0; y < H; ++y) {
+        for (int x = 0; x < W; ++x) {
+            int64_t out = INT64_MIN;
+            if (x >= 3 && x <= W - 4 && y >= 3 && y <= H - 4) {
+                int64_t sxx = 0, sxy = 0, syy = 0;
+                for (int j = -2; j <= 2; ++j) {
+                    for (int i = -2; i <= 2; ++i) {
+                        int u = x + i, v = y + j;
+                        int64_t A = (int64_t)img[(size_t)v * W + u + 1] - img[(size_t)v * W + u - 1];
+                        int64_t B = (int64_t)img[(size_t)(v + 1) * W + u] - img[(size_t)(v - 1) * W + u];
+                        int64_t w = (int64_t)b[i + 2] * b[j + 2];
+                        sxx += w * A * A;
+                        sxy += w * A * B;
+                        syy += w * B * B;
+                    }
+                }
+                out = 25 * (sxx * syy - sxy * sxy) - (sxx + syy) * (sxx + syy);
+            }
+            R25[(size_t)y * W + x] = out;
+        }
+    }
+    return OR_OK;
+}
+
+/* R-29: corners.  A pixel with 4 <= x <= W-5, 4 <= y <= H-5 is a corner iff
+ * R25 >= thr and R25 is strictly greater than all 8 neighbours'.  The
+ * image is cut into gc x gr cells, cell (i,j) = [floor(iW/gc), floor((i+1)W/gc)) x
+ * [floor(jH/gr), floor((j+1)H/gr)); each cell keeps its K corners of largest R25,
+ * ties to raster order (smaller y, then smaller x).  Output slots
+ * out[((j*gc + i)*K + rank)] = {x, y} and resp[...] = R25 for rank < count[j*gc+i];
+ * unused slots hold {-1, -1} and INT64_MIN.                                    */
+int oracle_harris_grid(const int64_t *R25, int W, int H, int gc, int gr, int K, int64_t thr,
+                       int32_t *out_xy, int64_t *resp, int32_t *count)
+{
+    if (!R25 || !out_xy || !resp || !count || W < 1 || H < 1 || gc < 1 || gr < 1 || K < 1 || thr < 1)
+        return OR_EINVAL;
+    for (int j = 0; j < gr; ++j) {
+        for (int i = 0; i < gc; ++i) {
+            const int cell = j * gc + i;
+            const int x0 = (int)((int64_t)i * W / gc), x1 = (int)((int64_t)(i + 1) * W / gc);
+            const int y0 = (int)((int64_t)j * H / gr), y1 = (int)((int64_t)(j + 1) * H / gr);
+            int n = 0;
+            for (int k = 0; k < K; ++k) {
+                out_xy[2 * ((size_t)cell * K + k)] = -1;
+                out_xy[2 * ((size_t)cell * K + k) + 1] = -1;
+                resp[(size_t)cell * K + k] = INT64_MIN;
+            }
+            /* raster scan; insertion into the sorted top-K keeps earlier (raster-first)
+             * entries ahead of later ones with equal response */
+            for (int y = y0; y < y1; ++y) {
+                for (int x = x0; x < x1; ++x) {
+                    if (x < 4 || x > W - 5 || y < 4 || y > H - 5) continue;
+                    int64_t r = R25[(size_t)y * W + x];
+                    if (r < thr) continue;
+                    int is_max = 1;
+                    for (int dy = -1; dy <= 1 && is_max; ++dy)
+                        for (int dx = -1; dx <= 1; ++dx) {
+                            if (!dx && !dy) continue;
+                            if (R25[(size_t)(y + dy) * W + x + dx] >= r) { is_max = 0; break; }
+                        }
+                    if (!is_max) continue;
+                    int pos = n < K ? n : K;
+                    while (pos > 0 && resp[(size_t)cell * K + pos - 1] < r) --pos;
+                    if (pos >= K) continue;
+                    for (int q = (n < K ? n : K - 1); q > pos; --q) {
+                        resp[(size_t)cell * K + q] = resp[(size_t)cell * K + q - 1];
+                        out_xy[2 * ((size_t)cell * K + q)] = out_xy[2 * ((size_t)cell * K + q - 1)];
+                        out_xy[2 * ((size_t)cell * K + q) + 1] = out_xy[2 * ((size_t)cell * K + q - 1) + 1];
+                    }
+                    resp[(size_t)cell * K + pos] = r;
+                    out_xy[2 * ((size_t)cell * K + pos)] = x;
+                    out_xy[2 * ((size_t)cell * K + pos) + 1] = y;
+                    if (n < K) ++n;
+                }
+            }
+            count[cell] = n;
+        }
+    }
+    return OR_OK;
+}
+
+/* R-30: zero-mean SSD ("ZSSD") of the (2r+1)^2 patches of img1 at
+ * (x1,y1) and img2 at (x2,y2), scaled by n = (2r+1)^2 to stay an integer:
+ *   cost = n * sum (a-b)^2 - (sum a - sum b)^2 = n * ZSSD,
+ *   ZSSD = sum ((a - mean a) - (b - mean b))^2.
+ * Patches must lie inside their images (else OR_EDIM).                         */
+int oracle_zssd(const uint8_t *img1, const uint8_t *img2, int W, int H, int x1, int y1, int x2, int y2, int r,
+                int64_t *cost)
+{
+    if (!img1 || !img2 || !cost || r < 1) return OR_EINVAL;
+    if (x1 < r || y1 < r || x1 + r >= W || y1 + r >= H) return OR_EDIM;
+    if (x2 < r || y2 < r || x2 + r >= W || y2 + r >= H) return OR_EDIM;
+    int64_t n = (int64_t)(2 * r + 1) * (2 * r + 1), sa = 0, sb = 0, sdd = 0;
+    for (int j = -r; j <= r; ++j)
+        for (int i = -r; i <= r; ++i) {
+            int64_t a = img1[(size_t)(y1 + j) * W + x1 + i], bb = img2[(size_t)(y2 + j) * W + x2 + i];
+            sa += a;
+            sb += bb;
+            sdd += (a - bb) * (a - bb);
+        }
+    *cost = n * sdd - (sa - sb) * (sa - sb);
+    return OR_OK;
+}
+
+/* R-31: match each corner of img1 into img2: candidates (x+dx, y+dy),
+ * |dx|,|dy| <= sr, patch inside img2; best = least cost, ties to raster order of
+ * the candidate; accepted iff cost <= max_cost and either no candidate lies at
+ * Chebyshev distance > 2 from the best, or 5*second > 6*best with second the least
+ * cost among those (the 1.2x ratio gate).  Corners whose img1 patch leaves the
+ * image, and unused slots (x < 0), are not matched.
+ * match[c] = {x2, y2} or {-1, -1}; mcost[c] = best cost (or -1).               */
+int oracle_zssd_match(const uint8_t *img1, const uint8_t *img2, int W, int H, const int32_t *xy, int ncorner,
+                      int r, int sr, int64_t max_cost, int32_t *match, int64_t *mcost)
+{
+    if (!img1 || !img2 || !xy || !match || !mcost || ncorner < 0 || r < 1 || sr < 1 || max_cost < 0) return OR_EINVAL;
+    for (int c = 0; c < ncorner; ++c) {
+        int x = xy[2 * c], y = xy[2 * c + 1];
+        match[2 * c] = match[2 * c + 1] = -1;
+        mcost[c] = -1;
+        if (x < r || y < r || x + r >= W || y + r >= H) continue;
+        int64_t best = INT64_MAX;
+        int bx = -1, by = -1;
+        for (int v = y - sr; v <= y + sr; ++v)
+            for (int u = x - sr; u <= x + sr; ++u) {
+                int64_t cst;
+                if (oracle_zssd(img1, img2, W, H, x, y, u, v, r, &cst) != OR_OK) continue;
+                if (cst < best) { best = cst; bx = u; by = v; }
+            }
+        if (bx < 0) continue;
+        int64_t second = INT64_MAX;
+        for (int v = y - sr; v <= y + sr; ++v)
+            for (int u = x - sr; u <= x + sr; ++u) {
+                int du = u - bx, dv = v - by;
+                if (du < 0) du = -du;
+                if (dv < 0) dv = -dv;
+                if ((du > dv ? du : dv) <= 2) continue;
+                int64_t cst;
+                if (oracle_zssd(img1, img2, W, H, x, y, u, v, r, &cst) != OR_OK) continue;
+                if (cst < second) second = cst;
+            }
+        int ok = best <= max_cost && (second == INT64_MAX || 5 * second > 6 * best);
+        if (ok) {
+            match[2 * c] = bx;
+            match[2 * c + 1] = by;
+            mcost[c] = best;
+        }
+    }
+    return OR_OK;
+}

@@ -449,3 +449,120 @@ def test_undistort_domain_rejects_runaway_maps():
     assert e.value.code == -3
     with pytest.raises(oracle.OracleError):
         oracle.undistort_map(64, 40, (0.0, 50.0, 31.5, 19.5, 0.0, 0.0, 0.0))
+
+
+# ----------------------------------------------------------------------------- f3 Harris + ZSSD
+I64_MIN = np.iinfo(np.int64).min
+
+
+def test_harris_closed_forms():
+    """R-28 pinned by closed forms of the binomial-window Harris response
+    (Eq.4-5): sum b = 16, sum b i^2 = 16 for b = {1,4,6,4,1}."""
+    H = W = 16
+    vv, uu = np.mgrid[0:H, 0:W]
+    R = oracle.harris_response(np.zeros((H, W), np.uint8))
+    assert (R[3:H - 3, 3:W - 3] == 0).all() and (R[:3] == I64_MIN).all() and (R[:, -3:] == I64_MIN).all()
+    # linear ramp I = 3x + 5y: A = 6, B = 10 everywhere -> det = 0, R25 = -(256 (36 + 100))^2
+    R = oracle.harris_response((3 * uu + 5 * vv).astype(np.uint8))
+    assert (R[3:H - 3, 3:W - 3] == -(256 * 136) ** 2).all()
+    # saddle I = x y: Sxx = 1024 (y^2+1), Syy = 1024 (x^2+1), Sxy = 1024 x y
+    R = oracle.harris_response((uu * vv).astype(np.uint8))
+    x, y = uu[3:H - 3, 3:W - 3].astype(np.int64), vv[3:H - 3, 3:W - 3].astype(np.int64)
+    expect = 25 * 1024 ** 2 * (x * x + y * y + 1) - 1024 ** 2 * (x * x + y * y + 2) ** 2
+    assert np.array_equal(R[3:H - 3, 3:W - 3], expect)
+
+
+def test_harris_rotation_invariance_and_edges():
+    rng = np.random.default_rng(21)
+    img = rng.integers(0, 256, size=(23, 23), dtype=np.uint8)
+    R = oracle.harris_response(img)
+    Rr = oracle.harris_response(np.ascontiguousarray(np.rot90(img)))
+    assert np.array_equal(np.rot90(R), Rr)                     # "invariant to rotation" (P:54)
+    step = np.zeros((20, 20), np.uint8)
+    step[:, 10:] = 200
+    assert (oracle.harris_response(step)[3:-3, 3:-3] <= 0).all()  # straight edge: R <= 0 (S:337)
+    quad = np.zeros((20, 20), np.uint8)
+    quad[10:, 10:] = 200
+    Rq = oracle.harris_response(quad)
+    iy, ix = np.unravel_index(np.argmax(np.where(Rq == I64_MIN, I64_MIN, Rq)), Rq.shape)
+    assert Rq[iy, ix] > 0 and abs(iy - 9.5) <= 1.5 and abs(ix - 9.5) <= 1.5  # a corner responds at the corner
+
+
+def test_harris_single_pixel():
+    img = np.zeros((41, 41), np.uint8)
+    img[20, 20] = 255
+    xy, resp, cnt = oracle.harris_grid(oracle.harris_response(img), 1, 1, 4, 1)
+    assert cnt[0] >= 1 and abs(xy[0, 0] - 20) <= 1 and abs(xy[0, 1] - 20) <= 1  # S:316
+
+
+def _brute_grid(R, gc, gr, K, thr):
+    H, W = R.shape
+    out = []
+    for j in range(gr):
+        for i in range(gc):
+            x0, x1 = i * W // gc, (i + 1) * W // gc
+            y0, y1 = j * H // gr, (j + 1) * H // gr
+            cand = []
+            for y in range(max(y0, 4), min(y1, H - 4)):
+                for x in range(max(x0, 4), min(x1, W - 4)):
+                    r = R[y, x]
+                    nb = R[y - 1:y + 2, x - 1:x + 2].copy()
+                    nb[1, 1] = I64_MIN
+                    if r >= thr and (nb < r).all():
+                        cand.append((-int(r), y, x))
+            cand.sort()
+            out.append([(x, y, -r) for r, y, x in cand[:K]])
+    return out
+
+
+@pytest.mark.parametrize("seed", range(6))
+def test_harris_grid_matches_brute_selection(seed):
+    """R-29: per-cell top-K strict maxima, ties to raster order -- against a sort."""
+    rng = np.random.default_rng(seed)
+    H, W = int(rng.integers(12, 40)), int(rng.integers(12, 40))
+    R = rng.integers(0, 6, size=(H, W)).astype(np.int64) * 10  # many ties
+    gc, gr, K = int(rng.integers(1, 5)), int(rng.integers(1, 5)), int(rng.integers(1, 4))
+    xy, resp, cnt = oracle.harris_grid(R, gc, gr, K, 10)
+    for c, want in enumerate(_brute_grid(R, gc, gr, K, 10)):
+        assert cnt[c] == len(want)
+        for k, (x, y, r) in enumerate(want):
+            assert (xy[c * K + k, 0], xy[c * K + k, 1], resp[c * K + k]) == (x, y, r)
+        assert (xy[c * K + len(want):(c + 1) * K] == -1).all()
+
+
+def test_zssd_definition_and_properties():
+    from fractions import Fraction
+    rng = np.random.default_rng(3)
+    a = rng.integers(0, 256, size=(15, 15), dtype=np.uint8)
+    b = rng.integers(0, 256, size=(15, 15), dtype=np.uint8)
+    r = 2
+    n = (2 * r + 1) ** 2
+    pa = a[5:10, 6:11].astype(int)
+    pb = b[4:9, 7:12].astype(int)
+    ma, mb = Fraction(int(pa.sum()), n), Fraction(int(pb.sum()), n)
+    z = sum(((Fraction(int(u)) - ma) - (Fraction(int(v)) - mb)) ** 2 for u, v in zip(pa.ravel(), pb.ravel()))
+    assert oracle.zssd(a, b, 8, 7, 9, 6, r) == n * z                          # S:320 definition
+    assert oracle.zssd(a, a, 8, 7, 8, 7, r) == 0                               # identical patches
+    c = np.clip(a.astype(int) + 17, 0, 255).astype(np.uint8)
+    a2 = np.clip(a, 0, 238).astype(np.uint8)
+    assert oracle.zssd(a2, (a2 + 17).astype(np.uint8), 8, 7, 8, 7, r) == 0     # bias invariance
+    assert oracle.zssd(a, b, 8, 7, 9, 6, r) == oracle.zssd(b, a, 9, 6, 8, 7, r)  # symmetry (S:336)
+    with pytest.raises(oracle.OracleError):
+        oracle.zssd(a, b, 1, 7, 9, 6, r)
+    del c
+
+
+def test_zssd_match_self_shift_and_textureless():
+    rng = np.random.default_rng(4)
+    img = rng.integers(0, 256, size=(40, 60), dtype=np.uint8)
+    xy = np.array([[20, 20], [30, 15], [12, 25], [-1, -1]], np.int32)
+    m, c = oracle.zssd_match(img, img, xy, 3, 8)
+    assert np.array_equal(m[:3], xy[:3]) and (c[:3] == 0).all() and (m[3] == -1).all()  # S:330 self-match
+    sh = np.roll(img, 7, axis=1)                                                  # img2(x+7) = img1(x)
+    m, c = oracle.zssd_match(img, sh, xy, 3, 8)
+    assert np.array_equal(m[:3], xy[:3] + [7, 0]) and (c[:3] == 0).all()        # S:331 shift by (7,0)
+    flat = np.full_like(img, 90)
+    m, c = oracle.zssd_match(img, flat, xy, 3, 8)
+    assert (m == -1).all()                                                         # S:332 ambiguity rejected
+    m, c = oracle.zssd_match(img, sh, xy, 3, 8, max_cost=0)
+    assert np.array_equal(m[:3], xy[:3] + [7, 0])
