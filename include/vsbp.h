@@ -183,6 +183,36 @@ int rectify_prep_batch(int n, const uint8_t *rgb_raw, int W_hi, int H_hi, const 
                        uint8_t *gray_lo, uint8_t *rgb_rect, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * harris_corners_batch -- row f3, Harris corners on a grid (§2.3 Eq.4-5;
+ * P:84 "a 30x30 grid ... Harris corners inside each grid individually"; SPEC
+ * S:310-316; R-28, R-29), for n grey images:
+ *   gray : u8 [n][H][W];  R25 : int64 [n][H][W] workspace/output: 25 * Harris
+ *          response (k = 0.04), INT64_MIN outside 3 <= x <= W-4, 3 <= y <= H-4
+ *   corners: the K strict 3x3 maxima with 25R >= thr and the largest response in
+ *          each of the gc x gr cells (ties to raster order):
+ *          xy : int32 [n][gr*gc*K][2], resp : int64 [n][gr*gc*K] (unused slots
+ *          {-1,-1} / INT64_MIN), count : int32 [n][gr*gc]
+ * W, H >= 9; 1 <= K <= 16; gc, gr >= 1; thr >= 1 (else VSBP_EINVAL).
+ * ------------------------------------------------------------------------- */
+int harris_corners_batch(int n, const uint8_t *gray, int W, int H, int gc, int gr, int K, long long thr,
+                         long long *R25, int32_t *xy, long long *resp, int32_t *count, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * zssd_match_batch -- row f3, ZSSD correspondence between two frames ("compute
+ * correspondence between frame I_t1 and I_t2 ... within the given search range ...
+ * ZSSD"; R-30, R-31), for n image pairs:
+ *   img1, img2 : u8 [n][H][W];  xy : int32 [n][ncorner][2] corners of img1 (slots
+ *   with x < 0 are skipped);  r : patch radius (1..7);  sr : search radius (1..64)
+ *   match : int32 [n][ncorner][2] matched position in img2 or {-1,-1};
+ *   cost  : int64 [n][ncorner] n*ZSSD of the match (n = (2r+1)^2) or -1.
+ * A match is the least cost over the (2sr+1)^2 window (patch inside img2), ties to
+ * raster order, kept iff cost <= max_cost and the least cost beyond Chebyshev
+ * distance 2 exceeds 1.2x it (5*second > 6*best) or does not exist.
+ * ------------------------------------------------------------------------- */
+int zssd_match_batch(int n, const uint8_t *img1, const uint8_t *img2, int W, int H, const int32_t *xy,
+                     int ncorner, int r, int sr, long long max_cost, int32_t *match, long long *cost, void *stream);
+
+/* ---------------------------------------------------------------------------
  * pair_summary_batch -- a8: for B pairs write summary[b] =
  *   {n_valid[b], sum of disp_lo[b], label hash of disp_lo[b], first_pair_id + b}.
  *   disp_lo : int32 [B][H][W]; n_valid : device uint64 [B]; summary : device [B].

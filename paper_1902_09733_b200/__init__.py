@@ -67,6 +67,10 @@ _EXPORTS = {
     "prep_downsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                         C.c_void_p]),
     "prep_downsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "harris_corners_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
+                                       C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "zssd_match_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
+                                   C.c_int, C.c_int, C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p]),
     "rectify_prep_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_void_p,
                                      C.c_void_p, C.c_void_p]),
     "pair_summary_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_uint64,
@@ -250,6 +254,48 @@ def rectify_prep(rgb_raw: torch.Tensor, cam, s: int, gray: torch.Tensor | None =
     if squeeze:
         return gray[0], (rect[0] if rect is not None else None)
     return gray, rect
+
+
+def harris_corners(gray: torch.Tensor, gc: int = 30, gr: int = 30, K: int = 4, thr: int = 10 ** 9, stream=None):
+    """Row f3 (Eq.4-5, P:84 30x30 grid): grey uint8 [n,H,W] (or [H,W]) ->
+    (R25 int64 [n,H,W], xy int32 [n,gr*gc*K,2], resp int64 [n,gr*gc*K], count int32
+    [n,gr*gc]).  R25 = 25 * Harris response (k = 0.04)."""
+    squeeze = gray.dim() == 2
+    if squeeze:
+        gray = gray.unsqueeze(0)
+    n, H, W = gray.shape
+    d = gray.device
+    R25 = torch.empty((n, H, W), dtype=torch.int64, device=d)
+    xy = torch.empty((n, gr * gc * K, 2), dtype=torch.int32, device=d)
+    resp = torch.empty((n, gr * gc * K), dtype=torch.int64, device=d)
+    cnt = torch.empty((n, gr * gc), dtype=torch.int32, device=d)
+    _check(lib().harris_corners_batch(n, _dev(gray, torch.uint8, "gray"), W, H, gc, gr, K, int(thr),
+                                      _dev(R25, torch.int64, "R25"), _dev(xy, torch.int32, "xy"),
+                                      _dev(resp, torch.int64, "resp"), _dev(cnt, torch.int32, "count"),
+                                      _stream(stream)), "harris_corners_batch")
+    if squeeze:
+        return R25[0], xy[0], resp[0], cnt[0]
+    return R25, xy, resp, cnt
+
+
+def zssd_match(img1: torch.Tensor, img2: torch.Tensor, xy: torch.Tensor, r: int = 5, sr: int = 16,
+               max_cost: int = 2 ** 62, stream=None):
+    """Row f3 (P:56 ZSSD within a search range): corners xy int32 [n,m,2] of img1 ->
+    (match int32 [n,m,2] or -1, cost int64 [n,m] = n*ZSSD or -1)."""
+    squeeze = img1.dim() == 2
+    if squeeze:
+        img1, img2, xy = img1.unsqueeze(0), img2.unsqueeze(0), xy.unsqueeze(0)
+    n, H, W = img1.shape
+    m = xy.shape[1]
+    match = torch.empty((n, m, 2), dtype=torch.int32, device=img1.device)
+    cost = torch.empty((n, m), dtype=torch.int64, device=img1.device)
+    _check(lib().zssd_match_batch(n, _dev(img1, torch.uint8, "img1"), _dev(img2, torch.uint8, "img2"), W, H,
+                                  _dev(xy, torch.int32, "xy"), m, r, sr, int(max_cost),
+                                  _dev(match, torch.int32, "match"), _dev(cost, torch.int64, "cost"),
+                                  _stream(stream)), "zssd_match_batch")
+    if squeeze:
+        return match[0], cost[0]
+    return match, cost
 
 
 def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.ndarray:

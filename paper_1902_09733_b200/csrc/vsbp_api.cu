@@ -553,6 +553,31 @@ int rectify_prep_batch(int n, const uint8_t *rgb_raw, int W_hi, int H_hi, const 
     return VSBP_OK;
 }
 
+int harris_corners_batch(int n, const uint8_t *gray, int W, int H, int gc, int gr, int K, long long thr,
+                         long long *R25, int32_t *xy, long long *resp, int32_t *count, void *stream)
+{
+    if (n < 1 || !gray || !R25 || !xy || !resp || !count || W < 9 || H < 9 || gc < 1 || gr < 1 || K < 1 || K > 16 ||
+        thr < 1)
+        return VSBP_EINVAL;
+    if ((long long)W * H > (1ll << 28) || (long long)gc * gr > (1ll << 24)) return VSBP_EINVAL;
+    CK(vsbp::launch_harris(n, gray, W, H, gc, gr, K, (int64_t)thr, (int64_t *)R25, xy, (int64_t *)resp, count,
+                           (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int zssd_match_batch(int n, const uint8_t *img1, const uint8_t *img2, int W, int H, const int32_t *xy,
+                     int ncorner, int r, int sr, long long max_cost, int32_t *match, long long *cost, void *stream)
+{
+    if (n < 1 || !img1 || !img2 || !xy || !match || !cost || W < 1 || H < 1 || ncorner < 0 || r < 1 || r > 7 ||
+        sr < 1 || sr > 64 || max_cost < 0)
+        return VSBP_EINVAL;
+    if ((long long)W * H > (1ll << 28)) return VSBP_EINVAL;
+    if (ncorner == 0) return VSBP_OK;
+    CK(vsbp::launch_zssd_match(n, img1, img2, W, H, xy, ncorner, r, sr, (int64_t)max_cost, match, (int64_t *)cost,
+                               (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
 int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsigned long long *n_valid,
                        uint64_t first_pair_id, vsbp_summary *summary, void *stream)
 {

@@ -70,3 +70,13 @@ bool rectify_domain_ok(int W, int H, const double *cam);
 cudaError_t launch_rectify_prep(int n, const uint8_t *raw, int W, int H, const double *cam, int s, uint8_t *gray,
                                 uint8_t *rect, cudaStream_t st);
 }  // namespace vsbp
+
+namespace vsbp {
+// row f3 (features.cu): Harris response + grid selection, ZSSD matching
+cudaError_t launch_harris(int n, const uint8_t *img, int W, int H, int gc, int gr, int K, int64_t thr, int64_t *R25,
+                          int32_t *xy, int64_t *resp, int32_t *count, cudaStream_t st);
+size_t zssd_smem(int r, int sr);
+cudaError_t launch_zssd_match(int n, const uint8_t *img1, const uint8_t *img2, int W, int H, const int32_t *xy,
+                              int ncorner, int r, int sr, int64_t max_cost, int32_t *match, int64_t *mcost,
+                              cudaStream_t st);
+}  // namespace vsbp

@@ -378,3 +378,54 @@ def test_pipeline_with_rectification_end_to_end():
     assert np.max(np.abs(pipe.disp_hi[0].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
     amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
     assert abs(int(summ[0, 0]) - n_o) <= amb
+
+
+# ----------------------------------------------------------------------------- f3
+@pytest.mark.parametrize("W,H,gc,gr,K,thr", [(64, 48, 4, 3, 4, 1), (97, 61, 30, 30, 4, 10 ** 6),
+                                             (33, 20, 2, 2, 16, 1), (676, 380, 30, 30, 4, 10 ** 9)])
+def test_harris_corners_bit_exact(W, H, gc, gr, K, thr):
+    imgs = [synthgen.value_noise_rgb(40 + i, W * 4, H * 4) for i in range(2)]
+    grey = np.stack([oracle.prep(im, 4) for im in imgs])
+    grey[1, 10:20, 10:30] = 128  # flat patch and ties
+    R, xy, resp, cnt = P.harris_corners(to_dev(grey), gc, gr, K, thr)
+    for i in range(2):
+        R_o = oracle.harris_response(grey[i])
+        assert np.array_equal(R[i].cpu().numpy(), R_o)
+        xy_o, resp_o, cnt_o = oracle.harris_grid(R_o, gc, gr, K, thr)
+        assert np.array_equal(cnt[i].cpu().numpy(), cnt_o)
+        assert np.array_equal(xy[i].cpu().numpy(), xy_o)
+        assert np.array_equal(resp[i].cpu().numpy(), resp_o)
+
+
+def test_harris_grid_ties_on_gpu():
+    """A plateau of equal responses: raster order decides, as in the oracle."""
+    img = np.zeros((40, 40), np.uint8)
+    for y in range(6, 34, 6):
+        for x in range(6, 34, 6):
+            img[y, x] = 200  # identical isolated peaks -> equal responses
+    R, xy, resp, cnt = P.harris_corners(to_dev(img), 2, 2, 3, 1)
+    xy_o, resp_o, cnt_o = oracle.harris_grid(oracle.harris_response(img), 2, 2, 3, 1)
+    assert np.array_equal(xy.cpu().numpy(), xy_o) and np.array_equal(cnt.cpu().numpy(), cnt_o)
+
+
+@pytest.mark.parametrize("r,sr", [(2, 4), (5, 16), (3, 12), (7, 20)])
+def test_zssd_match_bit_exact(r, sr):
+    left, right, _ = synthgen.stereo_pair_rgb(8)
+    g1, g2 = oracle.prep(left, 4)[:120, :200].copy(), oracle.prep(right, 4)[:120, :200].copy()
+    R = oracle.harris_response(g1)
+    xy, _, _ = oracle.harris_grid(R, 6, 4, 3, 10 ** 8)
+    m_g, c_g = P.zssd_match(to_dev(g1), to_dev(g2), to_dev(xy), r, sr, max_cost=2 ** 40)
+    m_o, c_o = oracle.zssd_match(g1, g2, xy, r, sr, max_cost=2 ** 40)
+    assert np.array_equal(m_g.cpu().numpy(), m_o)
+    assert np.array_equal(c_g.cpu().numpy(), c_o)
+    assert (m_o[:, 0] >= 0).sum() > 0
+
+
+def test_zssd_match_constructed_shift_on_gpu():
+    rng = np.random.default_rng(9)
+    img = rng.integers(0, 256, size=(60, 90), dtype=np.uint8)
+    sh = np.ascontiguousarray(np.roll(img, 7, axis=1))
+    xy = np.array([[30, 30], [45, 20], [20, 40], [-1, -1], [2, 2]], np.int32)
+    m, c = P.zssd_match(to_dev(img), to_dev(sh), to_dev(xy), 3, 8)
+    m = m.cpu().numpy()
+    assert np.array_equal(m[:3], xy[:3] + [7, 0]) and (m[3:] == -1).all()
