@@ -39,6 +39,7 @@ import numpy as np  # noqa: E402
 
 METRIC = "2.7K frame pairs/sec (disparity+point cloud) at 1/2/4/8 B200; HBM GB/s % peak"
 W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS = 2704, 1520, 4, 64, 5, 5
+FEATURES = dict(gc=30, gr=30, K=4, thr=10 ** 9, r=5, sr=48)  # f3 on the 676x380 grey pair (P:84 grid)
 CAMERA = (1400.0, 1400.0, 1351.5, 759.5, -0.25, 0.08, -0.01)  # f1: GoPro-like radial model
 WORKLOAD = ("C5 per GPU: stream of synthetic 2.7K RGB pairs, full pipeline a0-a8 "
             "(prep s=4 -> BP 676x380 L=64 5 levels x 5 iters -> JBU r=2 to 2704x1520 -> reproject -> summary)")
@@ -56,6 +57,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--cpu-pairs", type=int, default=4, help="oracle pairs per host thread (cpu_baseline)")
+    p.add_argument("--features", action="store_true",
+                   help="row f3: Harris corners (30x30 grid) on the left frame + ZSSD matching into the right")
     p.add_argument("--rectify", action="store_true",
                    help="row f1: undistort the raw frames (GoPro-like radial model) before a0")
     return p.parse_args()
@@ -240,7 +243,8 @@ def run_ours(args):
     I = q_intrinsics()
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS, batch=B, Q=Q, device=dev,
-                            camera=CAMERA if args.rectify else None)
+                            camera=CAMERA if args.rectify else None,
+                            features=FEATURES if args.features else None)
     pipe.bp.timing(True)
 
     # seeded synthetic pairs; rank r owns global batches r, r+N, ... (shard.py)
@@ -346,7 +350,8 @@ def run_ours(args):
             "metric": METRIC, "value": value, "unit": "pairs/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
-            "config": {"workload": WORKLOAD + (" + f1 undistortion of the raw frames" if args.rectify else ""),
+            "config": {"workload": WORKLOAD + (" + f1 undistortion of the raw frames" if args.rectify else "")
+                       + (" + f3 Harris/ZSSD correspondences (sr=48)" if args.features else ""),
                        "batch_per_gpu": B, "pairs_per_step": world * B,
                        "parallelism": f"dp{world} (pairs round-robin, NCCL all_gather of summaries)",
                        "l2": f"inputs larger than L2 ({(left_d.numel() + right_d.numel()) / 1e6:.0f} MB RGB + "

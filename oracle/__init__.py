@@ -58,6 +58,7 @@ def lib():
         L.oracle_undistort_map.argtypes = [i, i, p, p, p]
         L.oracle_remap_rgb.argtypes = [p, i, i, p, p, p]
         L.oracle_harris_response.argtypes = [p, i, i, p]
+        L.oracle_csbp.argtypes = [p, p, i, i, i, i, i, i, f, f, f, p, p]
         L.oracle_harris_grid.argtypes = [p, i, i, i, i, i, C.c_int64, p, p, p]
         L.oracle_zssd.argtypes = [p, p, i, i, i, i, i, i, i, p]
         L.oracle_zssd_match.argtypes = [p, p, i, i, p, i, i, i, C.c_int64, p, p]
@@ -154,6 +155,34 @@ def rectify_prep(rgb: np.ndarray, cam, s: int) -> tuple[np.ndarray, np.ndarray]:
     mx, my = undistort_map(W, H, cam)
     rect = remap_rgb(rgb, mx, my)
     return rect, prep(rect, s)
+
+
+def csbp_k(L: int, levels: int, k0: int) -> list[int]:
+    """R-32: candidates per level, k_l = min(L, k0 * 2^l)."""
+    return [min(L, k0 << l) for l in range(levels)]
+
+
+def csbp_disparity(left, right, L, levels, iters, k0, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
+                   return_candidates=False):
+    """f2 (P:30 [4] = constant-space BP, P:98; R-32..R-35): int32 labels [H][W];
+    with return_candidates also the per-level candidate lists [H_l][W_l][k_l]."""
+    left = np.ascontiguousarray(left, np.uint8)
+    right = np.ascontiguousarray(right, np.uint8)
+    H, W = left.shape
+    disp = np.zeros((H, W), np.int32)
+    dims = level_dims(W, H, levels)
+    ks = csbp_k(L, levels, k0)
+    tot = sum(w * h * k for (w, h), k in zip(dims, ks))
+    cand = np.zeros(max(tot, 1), np.int32)
+    _check(lib().oracle_csbp(_ptr(left), _ptr(right), W, H, L, levels, iters, k0, lam, data_trunc, disc_trunc,
+                             _ptr(disp), _ptr(cand) if return_candidates else None), "oracle_csbp")
+    if not return_candidates:
+        return disp
+    out, off = [], 0
+    for (w, h), k in zip(dims, ks):
+        out.append(cand[off:off + w * h * k].reshape(h, w, k))
+        off += w * h * k
+    return disp, out
 
 
 def harris_response(img: np.ndarray) -> np.ndarray:

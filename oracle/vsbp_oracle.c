@@ -762,3 +762,207 @@ int oracle_zssd_match(const uint8_t *img1, const uint8_t *img2, int W, int H, co
     }
     return OR_OK;
 }
+
+/* ------------------------------------------------------------------------- */
+/* F2  constant-space BP  ("GPU based Belief Propagation [4]", [4] = Yang, */
+/*     Wang, Ahuja, "A constant-space belief propagation algorithm for stereo   */
+/*     matching", CVPR 2010; R-32..R-35)                         */
+/*                                                                             */
+/* Same energy, quantisation, pyramid dims, checkerboard schedule and border   */
+/* rule as the full BP (R-1..R-12), but every pixel of level l keeps only      */
+/* k_l = min(L, k0 * 2^l) candidate labels (R-32), with messages over the      */
+/* receiver's candidates, stored at the receiver (in[p][k][i] = message p      */
+/* receives from its neighbour in direction k, for p's candidate i):           */
+/*  * top level T: candidates = the k_T labels of least D_T(p,.), ties to the  */
+/*    smaller label; incoming messages 0 (R-33);                               */
+/*  * level l < T, parent P = (x/2, y/2): pool = P's candidates; score(d) =    */
+/*    D_l(p,d) + sum_k in[P][k][d]; candidates = the k_l pool labels of least  */
+/*    score (ties to the smaller label); in[p][k][d] = in[P][k][d] if p has a  */
+/*    neighbour in direction k, else 0 (R-34);                                 */
+/*  * update of p toward existing neighbour q (direction k), labels c_p, c_q:  */
+/*      h(i) = D(p,c_p[i]) + sum_{k' != k} in[p][k'][i]                         */
+/*      m(j) = min( min_i h(i) + S |c_p[i] - c_q[j]|, min_i h(i) + tau_q )     */
+/*      in[q][opp(k)][j] = m(j) - min_j m(j)                     (R-35)         */
+/*  * WTA at level 0: the candidate of least D + sum_k in, ties to the smaller */
+/*    label.  Candidate lists are kept in ascending label order.               */
+/* D_l is the full-resolution data term summed over the pixel's footprint,    */
+/* i.e. the cost pyramid of O3.                                               */
+/* ------------------------------------------------------------------------- */
+
+/* indices of the k least values of score[0..n) (ties: smaller key), written in
+ * ascending key order (keys ascending in the input) */
+static void select_k(const int64_t *score, const int32_t *key, int n, int k, int32_t *out_idx)
+{
+    char *taken = (char *)calloc((size_t)n, 1);
+    int32_t *sel = (int32_t *)malloc(sizeof(int32_t) * (size_t)k);
+    for (int r = 0; r < k; ++r) {
+        int b = -1;
+        for (int i = 0; i < n; ++i) {
+            if (taken[i]) continue;
+            if (b < 0 || score[i] < score[b] || (score[i] == score[b] && key[i] < key[b])) b = i;
+        }
+        taken[b] = 1;
+        sel[r] = b;
+    }
+    /* ascending key order: keys of the input are ascending, so ascending index */
+    int w = 0;
+    for (int i = 0; i < n; ++i)
+        if (taken[i]) out_idx[w++] = i;
+    free(taken);
+    free(sel);
+}
+
+int oracle_csbp(const uint8_t *left, const uint8_t *right, int W, int H, int L, int levels, int iters, int k0,
+                float lambda, float data_trunc, float disc_trunc, int32_t *disp, int32_t *cand_out)
+{
+    if (!left || !right || !disp || W < 1 || H < 1 || L < 2 || levels < 1 || levels > 16 || iters < 1 || k0 < 1)
+        return OR_EINVAL;
+    int32_t q[4];
+    int rc = oracle_quantize(lambda, data_trunc, disc_trunc, q);
+    if (rc) return rc;
+    int32_t lam_q = q[0], tau_d = q[1], tau_q = q[2], S = q[3];
+    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q +
+                    ((int64_t)1 << 20);
+    if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
+    int Ws[16], Hs[16], K[16];
+    level_dims(W, H, levels, Ws, Hs);
+    for (int l = 0; l < levels; ++l) {
+        int64_t k = (int64_t)k0 << l;
+        K[l] = k < L ? (int)k : L;
+    }
+    int32_t *Dl[16] = {0}, *C[16] = {0}, *M[16] = {0};
+    rc = OR_OK;
+    for (int l = 0; l < levels; ++l) {
+        size_t n = (size_t)Ws[l] * Hs[l];
+        Dl[l] = (int32_t *)malloc(sizeof(int32_t) * n * L);
+        C[l] = (int32_t *)malloc(sizeof(int32_t) * n * K[l]);
+        M[l] = (int32_t *)calloc(n * 4 * K[l], sizeof(int32_t));
+        if (!Dl[l] || !C[l] || !M[l]) { rc = OR_EINVAL; goto done; }
+    }
+    rc = oracle_cost_volume(left, right, W, H, L, lam_q, tau_d, Dl[0]);
+    if (rc) goto done;
+    for (int l = 0; l + 1 < levels; ++l) {
+        rc = oracle_pyramid_down(Dl[l], Ws[l], Hs[l], L, Dl[l + 1]);
+        if (rc) goto done;
+    }
+    {
+        int64_t *score = (int64_t *)malloc(sizeof(int64_t) * (size_t)L);
+        int32_t *keys = (int32_t *)malloc(sizeof(int32_t) * (size_t)L);
+        int32_t *idx = (int32_t *)malloc(sizeof(int32_t) * (size_t)L);
+        int64_t *h = (int64_t *)malloc(sizeof(int64_t) * (size_t)L);
+        int64_t *m = (int64_t *)malloc(sizeof(int64_t) * (size_t)L);
+        for (int l = levels - 1; l >= 0; --l) {
+            const int w = Ws[l], hh = Hs[l], k = K[l];
+            /* candidates and initial messages (R-33, R-34) */
+            for (int y = 0; y < hh; ++y) {
+                for (int x = 0; x < w; ++x) {
+                    const size_t p = (size_t)y * w + x;
+                    int32_t *cp = C[l] + p * k;
+                    int32_t *mp = M[l] + p * 4 * k;
+                    const int32_t *Dp = Dl[l] + p * L;
+                    if (l == levels - 1) {
+                        for (int d = 0; d < L; ++d) {
+                            score[d] = Dp[d];
+                            keys[d] = d;
+                        }
+                        select_k(score, keys, L, k, idx);
+                        for (int i = 0; i < k; ++i) cp[i] = idx[i];
+                        /* messages stay 0 */
+                    } else {
+                        const int kp = K[l + 1], wp = Ws[l + 1];
+                        const size_t P = (size_t)(y / 2) * wp + (x / 2);
+                        const int32_t *cP = C[l + 1] + P * kp;
+                        const int32_t *mP = M[l + 1] + P * 4 * kp;
+                        for (int i = 0; i < kp; ++i) {
+                            int64_t s = Dp[cP[i]];
+                            for (int kk = 0; kk < 4; ++kk) s += mP[kk * kp + i];
+                            score[i] = s;
+                            keys[i] = cP[i];
+                        }
+                        select_k(score, keys, kp, k, idx);
+                        for (int i = 0; i < k; ++i) {
+                            cp[i] = cP[idx[i]];
+                            for (int kk = 0; kk < 4; ++kk) {
+                                int nx, ny;
+                                mp[kk * k + i] = neighbour(x, y, kk, w, hh, &nx, &ny) ? mP[kk * kp + idx[i]] : 0;
+                            }
+                        }
+                    }
+                }
+            }
+            /* checkerboard iterations (R-10, R-11, R-35) */
+            for (int t = 0; t < iters; ++t) {
+                for (int y = 0; y < hh; ++y) {
+                    for (int x = 0; x < w; ++x) {
+                        if (((x + y + t) & 1) != 0) continue;
+                        const size_t p = (size_t)y * w + x;
+                        const int32_t *cp = C[l] + p * k;
+                        const int32_t *mp = M[l] + p * 4 * k;
+                        const int32_t *Dp = Dl[l] + p * L;
+                        for (int kk = 0; kk < 4; ++kk) {
+                            int nx, ny;
+                            if (!neighbour(x, y, kk, w, hh, &nx, &ny)) continue;
+                            const size_t qq = (size_t)ny * w + nx;
+                            const int32_t *cq = C[l] + qq * k;
+                            int64_t hmin = INT64_MAX;
+                            for (int i = 0; i < k; ++i) {
+                                int64_t s = Dp[cp[i]];
+                                for (int k2 = 0; k2 < 4; ++k2)
+                                    if (k2 != kk) s += mp[k2 * k + i];
+                                h[i] = s;
+                                if (s < hmin) hmin = s;
+                            }
+                            int64_t mmin = INT64_MAX;
+                            for (int j = 0; j < k; ++j) {
+                                int64_t best = hmin + tau_q;
+                                for (int i = 0; i < k; ++i) {
+                                    int64_t dd = cp[i] - cq[j];
+                                    if (dd < 0) dd = -dd;
+                                    int64_t v = h[i] + (int64_t)S * dd;
+                                    if (v < best) best = v;
+                                }
+                                m[j] = best;
+                                if (best < mmin) mmin = best;
+                            }
+                            int32_t *dst = M[l] + qq * 4 * k + (size_t)opposite(kk) * k;
+                            for (int j = 0; j < k; ++j) dst[j] = (int32_t)(m[j] - mmin);
+                        }
+                    }
+                }
+            }
+        }
+        /* WTA (R-35) */
+        for (int y = 0; y < H; ++y) {
+            for (int x = 0; x < W; ++x) {
+                const size_t p = (size_t)y * W + x;
+                const int k = K[0];
+                const int32_t *cp = C[0] + p * k;
+                const int32_t *mp = M[0] + p * 4 * k;
+                int64_t best = INT64_MAX;
+                int lab = 0;
+                for (int i = 0; i < k; ++i) {
+                    int64_t s = Dl[0][p * L + cp[i]];
+                    for (int kk = 0; kk < 4; ++kk) s += mp[kk * k + i];
+                    if (s < best) { best = s; lab = cp[i]; }  /* ascending labels: first = smaller */
+                }
+                disp[p] = lab;
+            }
+        }
+        free(score);
+        free(keys);
+        free(idx);
+        free(h);
+        free(m);
+    }
+    if (cand_out) {
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            size_t n = (size_t)Ws[l] * Hs[l] * K[l];
+            memcpy(cand_out + off, C[l], sizeof(int32_t) * n);
+            off += n;
+        }
+    }
+done:
+    for (int l = 0; l < levels; ++l) { free(Dl[l]); free(C[l]); free(M[l]); }
+    return rc;
+}

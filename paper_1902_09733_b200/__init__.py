@@ -376,7 +376,7 @@ class StereoPipeline:
 
     def __init__(self, W_hi, H_hi, s, ndisp, levels, iters, batch, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
                  sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0,
-                 camera=None):
+                 camera=None, features=None):
         self.W_hi, self.H_hi, self.s, self.B = W_hi, H_hi, s, batch
         self.W, self.H = W_hi // s, H_hi // s
         self.sigma_s = 15.0 / s if sigma_s is None else sigma_s  # R-16
@@ -396,6 +396,10 @@ class StereoPipeline:
         # row f1: with a camera (f_u, f_v, c_u, c_v, k1, k2, k3) the raw frames are
         # undistorted first (fused with a0); the rectified left frame is the JBU guide
         self.camera = camera
+        # row f3: features = dict(gc, gr, K, thr, r, sr[, max_cost]) runs Harris on the
+        # left grey frame and ZSSD-matches the corners into the right one
+        self.features = features
+        self.corners = self.matches = None
         self.rect = (torch.empty((batch, H_hi, W_hi, 3), dtype=torch.uint8, device=dev)
                      if camera is not None else None)
 
@@ -412,6 +416,13 @@ class StereoPipeline:
             prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
             guide = left_rgb
         self.bp.disparity(self.gray[0, :B], self.gray[1, :B], out=self.disp[:B], stream=stream)
+        if self.features is not None:
+            f = self.features
+            _, xy, _, _ = harris_corners(self.gray[0, :B], f.get("gc", 30), f.get("gr", 30), f.get("K", 4),
+                                         f.get("thr", 10 ** 9), stream=stream)
+            self.corners = xy
+            self.matches = zssd_match(self.gray[0, :B], self.gray[1, :B], xy, f.get("r", 5), f.get("sr", 16),
+                                      f.get("max_cost", 2 ** 62), stream=stream)
         jbu_reproject(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
                       self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
                       stream=stream)

@@ -10,10 +10,10 @@
 //   * k_harris_grid: one CTA per grid cell keeps the K strict 3x3 maxima with the
 //     largest response (ties to raster order) -- per-thread sorted lists merged by
 //     one warp;
-//   * k_zssd_match: one CTA per corner stages its patch and the search window in
-//     shared memory, evaluates n*ZSSD = n sum (a-b)^2 - (sum a - sum b)^2 at every
-//     candidate (exact int32), takes the least cost (ties to raster order), then the
-//     least cost beyond Chebyshev distance 2 for the 1.2x ratio gate.
+//   * k_zssd_match: one CTA per corner stages the search window in shared memory,
+//     evaluates n*ZSSD = n sum (a-b)^2 - (sum a - sum b)^2 at every candidate with
+//     packed IDP4A correlation (exact), takes the least cost (ties to raster order),
+//     then the least cost beyond Chebyshev distance 2 for the 1.2x ratio gate.
 #include <stdint.h>
 
 #include "vsbp_internal.cuh"
@@ -191,13 +191,21 @@ __global__ void __launch_bounds__(HG_T) k_harris_grid(const int64_t *__restrict_
 }
 
 // ---------------------------------------------------------------- ZSSD matching
+// One CTA per corner.  The patch rows of img1 are packed into registers (P bytes per
+// row in ceil(P/4) words, zero-padded); the search window of img2 sits in shared
+// memory with a row pitch that is a multiple of 4.  A work item is one candidate
+// row dy and 4 consecutive dx: per patch row it loads the covering words once and,
+// per candidate, aligns them with PRMT and accumulates sum(ab), sum(b), sum(b^2) with
+// IDP4A (u8 x u8 -> u32, exact).  n*ZSSD = n (Sa2 - 2 Sab + Sb2) - (Sa - Sb)^2.
 constexpr int ZM_T = 256;
 
+template <int R>
 __global__ void __launch_bounds__(ZM_T) k_zssd_match(const uint8_t *__restrict__ img1, const uint8_t *__restrict__ img2,
-                                                     int W, int H, const int32_t *__restrict__ xy, int ncorner, int r,
-                                                     int sr, int64_t max_cost, int32_t *__restrict__ match,
+                                                     int W, int H, const int32_t *__restrict__ xy, int ncorner, int sr,
+                                                     int64_t max_cost, int32_t *__restrict__ match,
                                                      int64_t *__restrict__ mcost)
 {
+    constexpr int P = 2 * R + 1, n = P * P, NWP = (P + 3) / 4;  // words per patch row
     extern __shared__ __align__(16) unsigned char zsm[];
     const int b = blockIdx.y, c = blockIdx.x;
     const size_t cs = (size_t)b * ncorner + c;
@@ -206,45 +214,79 @@ __global__ void __launch_bounds__(ZM_T) k_zssd_match(const uint8_t *__restrict__
         match[2 * cs] = match[2 * cs + 1] = -1;
         mcost[cs] = -1;
     }
-    if (x < r || y < r || x + r >= W || y + r >= H) return;
-    const int P = 2 * r + 1, n = P * P;
-    const int S = 2 * sr + 1;          // candidate grid side
-    const int RW = S + 2 * r;          // staged img2 window side
-    uint8_t *pa = zsm;                 // [P][P]
-    uint8_t *rb = zsm + n;             // [RW][RW], out-of-image bytes never used
-    unsigned *cost = reinterpret_cast<unsigned *>(zsm + ((n + RW * RW + 15) & ~15));  // [S][S], ~0 = invalid
+    if (x < R || y < R || x + R >= W || y + R >= H) return;
+    const int S = 2 * sr + 1;                       // candidate grid side
+    const int RW = S + 2 * R, RP = (RW + 3 + 8) & ~3;  // staged img2 window, padded pitch
+    uint8_t *rb = zsm;                              // [RW][RP]
+    unsigned *cost = reinterpret_cast<unsigned *>(zsm + (size_t)RW * RP);  // [S][S], ~0 = invalid
     const uint8_t *I1 = img1 + (size_t)b * W * H, *I2 = img2 + (size_t)b * W * H;
-    for (int e = threadIdx.x; e < n; e += ZM_T) pa[e] = __ldg(I1 + (size_t)(y - r + e / P) * W + (x - r + e % P));
-    const int wx0 = x - sr - r, wy0 = y - sr - r;
-    for (int e = threadIdx.x; e < RW * RW; e += ZM_T) {
-        const int u = wx0 + e % RW, v = wy0 + e / RW;
-        rb[e] = (u >= 0 && v >= 0 && u < W && v < H) ? __ldg(I2 + (size_t)v * W + u) : 0;
+    const int wx0 = x - sr - R, wy0 = y - sr - R;
+    for (int e = threadIdx.x; e < RW * RP; e += ZM_T) {
+        const int lx = e % RP, ly = e / RP;
+        const int u = wx0 + lx, v = wy0 + ly;
+        rb[e] = (lx < RW && u >= 0 && v >= 0 && u < W && v < H) ? __ldg(I2 + (size_t)v * W + u) : 0;
     }
-    __syncthreads();
-    int sa = 0;
-    for (int e = 0; e < n; ++e) sa += pa[e];
-    // costs and the best candidate (cost, raster index) as one 64-bit key
-    unsigned long long best = ~0ull;
-    for (int e = threadIdx.x; e < S * S; e += ZM_T) {
-        const int dy = e / S, dx = e - dy * S;
-        const int u = x - sr + dx, v = y - sr + dy;
-        unsigned cst = 0xffffffffu;
-        if (u >= r && v >= r && u + r < W && v + r < H) {
-            int sb = 0, sdd = 0;
-            for (int j = 0; j < P; ++j) {
-                const uint8_t *ra = pa + j * P, *rr = rb + (dy + j) * RW + dx;
-                for (int i = 0; i < P; ++i) {
-                    const int bb = rr[i], d = (int)ra[i] - bb;
-                    sb += bb;
-                    sdd += d * d;
+    // the patch of img1, packed; sum a and sum a^2
+    unsigned pa[P][NWP];
+    int sa = 0, sa2 = 0;
+#pragma unroll
+    for (int j = 0; j < P; ++j)
+#pragma unroll
+        for (int q = 0; q < NWP; ++q) {
+            unsigned w = 0u;
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                if (4 * q + k < P) {
+                    const unsigned v = __ldg(I1 + (size_t)(y - R + j) * W + (x - R + 4 * q + k));
+                    w |= v << (8 * k);
+                    sa += (int)v;
+                    sa2 += (int)(v * v);
                 }
             }
-            // n * ZSSD < 2^32 for r <= 7 (225 * 225 * 65025)
-            cst = (unsigned)((int64_t)n * sdd - (int64_t)(sa - sb) * (sa - sb));
-            const unsigned long long key = ((unsigned long long)cst << 32) | (unsigned)e;
-            best = key < best ? key : best;
+            pa[j][q] = w;
         }
-        cost[e] = cst;
+    __syncthreads();
+    const unsigned lastmask = (P % 4) ? (0xFFFFFFFFu >> (8 * (4 - P % 4))) : 0xFFFFFFFFu;
+    const int G4 = (S + 3) / 4;
+    unsigned long long best = ~0ull;
+    for (int it = threadIdx.x; it < S * G4; it += ZM_T) {
+        const int dy = it / G4, dx0 = 4 * (it - dy * G4);
+        unsigned sab[4] = {0u, 0u, 0u, 0u}, sb[4] = {0u, 0u, 0u, 0u}, sb2[4] = {0u, 0u, 0u, 0u};
+#pragma unroll
+        for (int j = 0; j < P; ++j) {
+            const uint8_t *row = rb + (dy + j) * RP + dx0;  // dx0 % 4 == 0, RP % 4 == 0: aligned
+            const unsigned *wrow = reinterpret_cast<const unsigned *>(row);
+            unsigned w[NWP + 1];
+#pragma unroll
+            for (int q = 0; q <= NWP; ++q) w[q] = wrow[q];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+#pragma unroll
+                for (int q = 0; q < NWP; ++q) {
+                    unsigned bw = __byte_perm(w[q], w[q + 1], 0x3210 + 0x1111 * k);
+                    if (q == NWP - 1) bw &= lastmask;
+                    sab[k] = __dp4a(pa[j][q], bw, sab[k]);
+                    sb[k] = __dp4a(0x01010101u, bw, sb[k]);
+                    sb2[k] = __dp4a(bw, bw, sb2[k]);
+                }
+            }
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            const int dx = dx0 + k;
+            if (dx >= S) break;
+            const int u = x - sr + dx, v = y - sr + dy;
+            unsigned cst = 0xffffffffu;
+            if (u >= R && v >= R && u + R < W && v + R < H) {
+                const int64_t sdd = (int64_t)sa2 - 2 * (int64_t)sab[k] + (int64_t)sb2[k];
+                const int64_t dm = (int64_t)sa - (int64_t)sb[k];
+                cst = (unsigned)((int64_t)n * sdd - dm * dm);  // < 2^32 for R <= 7
+                const int e = dy * S + dx;
+                const unsigned long long key = ((unsigned long long)cst << 32) | (unsigned)e;
+                best = key < best ? key : best;
+            }
+            cost[dy * S + dx] = cst;
+        }
     }
     __shared__ unsigned long long wbest[ZM_T / 32];
     for (int o = 16; o > 0; o >>= 1) {
@@ -259,7 +301,7 @@ __global__ void __launch_bounds__(ZM_T) k_zssd_match(const uint8_t *__restrict__
     const int be = (int)(best & 0xffffffffu);
     const unsigned bcost = (unsigned)(best >> 32);
     const int bdy = be / S, bdx = be - bdy * S;
-    // the least cost beyond Chebyshev distance 2 of the best
+    // the least cost beyond Chebyshev distance 2 of the best (1.2x ratio gate)
     unsigned sec = 0xffffffffu;
     for (int e = threadIdx.x; e < S * S; e += ZM_T) {
         const int dy = e / S, dx = e - dy * S;
@@ -268,7 +310,6 @@ __global__ void __launch_bounds__(ZM_T) k_zssd_match(const uint8_t *__restrict__
     }
     __shared__ unsigned wsec[ZM_T / 32];
     for (int o = 16; o > 0; o >>= 1) sec = min(sec, __shfl_xor_sync(FULL, sec, o));
-    __syncthreads();  // wbest reads done before wsec writes share the barrier pattern
     if ((threadIdx.x & 31) == 0) wsec[threadIdx.x >> 5] = sec;
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -296,8 +337,8 @@ cudaError_t launch_harris(int n, const uint8_t *img, int W, int H, int gc, int g
 
 size_t zssd_smem(int r, int sr)
 {
-    const int P = 2 * r + 1, S = 2 * sr + 1, RW = S + 2 * r;
-    return (((size_t)P * P + (size_t)RW * RW + 15) & ~(size_t)15) + (size_t)S * S * sizeof(int);
+    const int S = 2 * sr + 1, RW = S + 2 * r, RP = (RW + 3 + 8) & ~3;
+    return (size_t)RW * RP + (size_t)S * S * sizeof(unsigned);
 }
 
 cudaError_t launch_zssd_match(int n, const uint8_t *img1, const uint8_t *img2, int W, int H, const int32_t *xy,
@@ -305,11 +346,21 @@ cudaError_t launch_zssd_match(int n, const uint8_t *img1, const uint8_t *img2, i
                               cudaStream_t st)
 {
     const size_t smem = zssd_smem(r, sr);
-    if (smem > 48 * 1024) {
-        cudaError_t e = cudaFuncSetAttribute(k_zssd_match, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e != cudaSuccess) return e;
+    const dim3 grid(ncorner, n);
+    cudaError_t e = cudaSuccess;
+#define VSBP_Z(R_)                                                                                             \
+    case R_:                                                                                                   \
+        if (smem > 48 * 1024)                                                                                  \
+            e = cudaFuncSetAttribute(k_zssd_match<R_>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (e == cudaSuccess)                                                                                  \
+            k_zssd_match<R_><<<grid, ZM_T, smem, st>>>(img1, img2, W, H, xy, ncorner, sr, max_cost, match, mcost); \
+        break;
+    switch (r) {
+        VSBP_Z(1) VSBP_Z(2) VSBP_Z(3) VSBP_Z(4) VSBP_Z(5) VSBP_Z(6) VSBP_Z(7)
+    default: return cudaErrorInvalidValue;
     }
-    k_zssd_match<<<dim3(ncorner, n), ZM_T, smem, st>>>(img1, img2, W, H, xy, ncorner, r, sr, max_cost, match, mcost);
+#undef VSBP_Z
+    if (e != cudaSuccess) return e;
     note_launch();
     return cudaGetLastError();
 }

@@ -429,3 +429,20 @@ def test_zssd_match_constructed_shift_on_gpu():
     m, c = P.zssd_match(to_dev(img), to_dev(sh), to_dev(xy), 3, 8)
     m = m.cpu().numpy()
     assert np.array_equal(m[:3], xy[:3] + [7, 0]) and (m[3:] == -1).all()
+
+
+def test_pipeline_features_match_oracle():
+    """f3 inside the pipeline: corners of the left grey frame and their ZSSD matches
+    in the right one equal the oracle's."""
+    left, right, _ = synthgen.stereo_pair_rgb(10)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    feats = dict(gc=8, gr=6, K=2, thr=10 ** 9, r=4, sr=20)
+    pipe = P.StereoPipeline(2704, 1520, 4, 64, 5, 5, batch=1, Q=Q, device=dev(), features=feats)
+    pipe.run(to_dev(left[None]), to_dev(right[None]))
+    gl, gr = oracle.prep(left, 4), oracle.prep(right, 4)
+    xy_o, _, _ = oracle.harris_grid(oracle.harris_response(gl), 8, 6, 2, 10 ** 9)
+    m_o, c_o = oracle.zssd_match(gl, gr, xy_o, 4, 20)
+    assert np.array_equal(pipe.corners[0].cpu().numpy(), xy_o)
+    assert np.array_equal(pipe.matches[0][0].cpu().numpy(), m_o)
+    assert np.array_equal(pipe.matches[1][0].cpu().numpy(), c_o)

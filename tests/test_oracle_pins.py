@@ -566,3 +566,71 @@ def test_zssd_match_self_shift_and_textureless():
     assert (m == -1).all()                                                         # S:332 ambiguity rejected
     m, c = oracle.zssd_match(img, sh, xy, 3, 8, max_cost=0)
     assert np.array_equal(m[:3], xy[:3] + [7, 0])
+
+
+# ----------------------------------------------------------------------------- f2 constant-space BP
+@pytest.mark.parametrize("seed", range(12))
+def test_csbp_single_level_all_labels_is_bp(seed):
+    """R-32..R-35 with one level and k >= L: every label is a candidate, messages are
+    the O(k^2) minimisation -- the full BP of O4 (Eq.1), label for label."""
+    rng = np.random.default_rng(300 + seed)
+    W, H, L = int(rng.integers(1, 14)), int(rng.integers(1, 10)), int(rng.integers(2, 12))
+    l = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    it = int(rng.integers(1, 8))
+    assert np.array_equal(oracle.csbp_disparity(l, r, L, 1, it, L + int(rng.integers(0, 3))),
+                          oracle.bp_disparity(l, r, L, 1, it))
+
+
+@pytest.mark.parametrize("seed", range(10))
+def test_csbp_chain_reaches_a_map_labelling(seed):
+    """On a chain (tree) BP converges to the exact min-marginals whatever the
+    coarse-level initialisation, so with all labels kept the WTA labelling has the
+    exhaustive minimum energy (unique-MAP draws)."""
+    rng = np.random.default_rng(400 + seed)
+    W, L = int(rng.integers(3, 8)), 3
+    l = rng.integers(0, 256, size=(1, W), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(1, W), dtype=np.uint8)
+    q = oracle.quantize(0.07, 15.0, 1.7)
+    D = oracle.cost_volume(l, r, L, q)
+    best, _ = exhaustive_map(D, q.S, q.tau_q)
+    f = oracle.csbp_disparity(l, r, L, 3, 2 * W + 4, L)
+    assert energy(D, f, q.S, q.tau_q) == best
+
+
+def test_csbp_candidates_selection_and_nesting():
+    rng = np.random.default_rng(7)
+    H, W, L, levels, k0 = 21, 30, 24, 3, 3
+    l = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    _, cands = oracle.csbp_disparity(l, r, L, levels, 4, k0, return_candidates=True)
+    ks = oracle.csbp_k(L, levels, k0)
+    assert [c.shape[2] for c in cands] == ks == [3, 6, 12]
+    q = oracle.quantize(0.07, 15.0, 1.7)
+    D = oracle.cost_volume(l, r, L, q)
+    for _ in range(levels - 1):
+        D = oracle.pyramid_down(D)
+    # top level: the k least data costs, ties to the smaller label (stable sort)
+    top = np.sort(np.argsort(D, axis=2, kind="stable")[:, :, :ks[-1]], axis=2)
+    assert np.array_equal(cands[-1], top)
+    for lv in range(levels - 1):
+        c, cp = cands[lv], cands[lv + 1]
+        assert (np.diff(c, axis=2) > 0).all()  # ascending, distinct
+        for y in range(c.shape[0]):
+            for x in range(c.shape[1]):
+                assert set(c[y, x]) <= set(cp[y // 2, x // 2])  # nested in the parent's (R-34)
+
+
+def test_csbp_recovers_constant_and_row_plane_shift():
+    l, r = synthgen.shifted_pair(1, 64, 48, 5)
+    d = oracle.csbp_disparity(l, r, 16, 3, 5, 2)
+    assert np.mean(d[:, 5:] == 5) >= 0.999
+    l, r, drow = synthgen.row_plane_pair(2, 160, 120, 4, 27)
+    disp = oracle.csbp_disparity(l, r, 32, 4, 5, 2)
+    truth = np.broadcast_to(drow[:, None], disp.shape)
+    step = np.zeros(120, bool)
+    step[1:] |= drow[1:] != drow[:-1]
+    step[:-1] |= drow[1:] != drow[:-1]
+    valid = (np.arange(160)[None, :] >= 40) & ~step[:, None]
+    frac = np.mean(disp[valid] == truth[valid])
+    assert frac >= 0.99, frac
