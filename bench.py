@@ -57,6 +57,8 @@ def parse():
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-threads", type=int, default=0)
     p.add_argument("--cpu-pairs", type=int, default=4, help="oracle pairs per host thread (cpu_baseline)")
+    p.add_argument("--csbp", type=int, default=0, metavar="K0",
+                   help="row f2: constant-space BP with k_l = min(L, K0 2^l) candidates instead of the full BP")
     p.add_argument("--features", action="store_true",
                    help="row f3: Harris corners (30x30 grid) on the left frame + ZSSD matching into the right")
     p.add_argument("--rectify", action="store_true",
@@ -244,8 +246,10 @@ def run_ours(args):
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS, batch=B, Q=Q, device=dev,
                             camera=CAMERA if args.rectify else None,
-                            features=FEATURES if args.features else None)
-    pipe.bp.timing(True)
+                            features=FEATURES if args.features else None, csbp_k0=args.csbp or None)
+    full_bp = isinstance(pipe.bp, P.StereoBP)
+    if full_bp:
+        pipe.bp.timing(True)
 
     # seeded synthetic pairs; rank r owns global batches r, r+N, ... (shard.py)
     pool_n = max(1, min(args.pool, B))
@@ -277,7 +281,8 @@ def run_ours(args):
 
     for s in range(args.warmup):
         step(s, left_d, right_d)
-    pipe.bp.timing_read()  # discard warm-up timings
+    if full_bp:
+        pipe.bp.timing_read()  # discard warm-up timings
     barrier()
 
     sampler = ClockSampler(local)
@@ -295,7 +300,7 @@ def run_ours(args):
     clocks = sampler.stop()
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms)
-    lv = pipe.bp.timing_read()
+    lv = pipe.bp.timing_read() if full_bp else None
     pairs = world * B * args.steps
     value = pairs / (ms_max / 1000.0)
 
@@ -319,23 +324,26 @@ def run_ours(args):
                "h2d_bytes_per_step": int(left_h.numel() + right_h.numel()),
                "d2h_bytes_per_step": int(runner.summary_host.numel() * 8),
                "overlap": "H2D of batch i+1 on a copy stream during compute of batch i"}
-        pipe.bp.timing_read()
+        if full_bp:
+            pipe.bp.timing_read()
 
     # ---- roofline of the dominant kernel: level-0 message updates (a4)
     peak, peak_kind = measured_peaks()
-    l0 = lv[0]
-    achieved = (l0["bytes"] / 1e9) / (l0["ms"] / 1e3) if l0["ms"] > 0 else 0.0
-    all_bytes = sum(x["bytes"] for x in lv)
-    all_ms = sum(x["ms"] for x in lv)
-    roofline = {
-        "kernel": "k_update (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
-        "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
-        "traffic": ncu_traffic(B),
-        "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
-        "us_per_launch": 1000.0 * l0["ms"] / max(l0["launches"], 1),
-        "share_of_step": all_ms / (ms if ms > 0 else 1.0),
-        "all_levels_gbs": (all_bytes / 1e9) / (all_ms / 1e3) if all_ms > 0 else 0.0,
-    }
+    roofline = None
+    if full_bp:
+        l0 = lv[0]
+        achieved = (l0["bytes"] / 1e9) / (l0["ms"] / 1e3) if l0["ms"] > 0 else 0.0
+        all_bytes = sum(x["bytes"] for x in lv)
+        all_ms = sum(x["ms"] for x in lv)
+        roofline = {
+            "kernel": "k_update (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+            "traffic": ncu_traffic(B),
+            "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
+            "us_per_launch": 1000.0 * l0["ms"] / max(l0["launches"], 1),
+            "share_of_step": all_ms / (ms if ms > 0 else 1.0),
+            "all_levels_gbs": (all_bytes / 1e9) / (all_ms / 1e3) if all_ms > 0 else 0.0,
+        }
 
     # ---- CPU baseline: the oracle on this host's cores (rank 0 at N=1 only)
     cpu = None
@@ -351,16 +359,17 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": ms_max / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
             "config": {"workload": WORKLOAD + (" + f1 undistortion of the raw frames" if args.rectify else "")
-                       + (" + f3 Harris/ZSSD correspondences (sr=48)" if args.features else ""),
+                       + (" + f3 Harris/ZSSD correspondences (sr=48)" if args.features else "")
+                       + (f" with f2 constant-space BP (k0={args.csbp})" if args.csbp else ""),
                        "batch_per_gpu": B, "pairs_per_step": world * B,
                        "parallelism": f"dp{world} (pairs round-robin, NCCL all_gather of summaries)",
                        "l2": f"inputs larger than L2 ({(left_d.numel() + right_d.numel()) / 1e6:.0f} MB RGB + "
                              f"{pipe.bp.workspace.numel() / 1e6:.0f} MB BP state per step)",
-                       "bp_msg_storage": f"u{8 * pipe.bp.params()['msg_bytes']}",
+                       "bp_msg_storage": f"u{8 * pipe.bp.params()['msg_bytes']}" if full_bp else "i32 (csbp)",
                        "jbu_arith": "f32"},
             "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu,
-            "per_level_update_ms_per_step": [x["ms"] / args.steps for x in lv],
+            "per_level_update_ms_per_step": [x["ms"] / args.steps for x in lv] if lv else None,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

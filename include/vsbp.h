@@ -183,6 +183,32 @@ int rectify_prep_batch(int n, const uint8_t *rgb_raw, int W_hi, int H_hi, const 
                        uint8_t *gray_lo, uint8_t *rgb_rect, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * Constant-space BP -- row f2, the BP the paper cites as [4] ("GPU based
+ * Belief Propagation [4]"; [4] = Yang, Wang, Ahuja, CVPR 2010; R-32..R-35).
+ * Same energy, quantisation, pyramid and checkerboard schedule as bp_create's BP,
+ * but level l keeps only k_l = min(ndisp, k0 * 2^l) candidate labels per pixel:
+ * the workspace is O(k) per pixel instead of O(ndisp) and the data term of a
+ * candidate is computed from the images on demand.
+ *   csbp_create     : arguments as bp_create plus k0 >= 1; VSBP_EINVAL if any
+ *                     k_l > 64; VSBP_EOVERFLOW as bp_create.  Host-only.
+ *   csbp_workspace_bytes / csbp_set_workspace : as the bp_ equivalents (caller-
+ *                     owned device memory, 256-byte aligned).
+ *   csbp_disparity_batch : left, right u8 [B][H][W] -> disp int32 [B][H][W] labels;
+ *                     async on `stream`.
+ *   csbp_get_candidates : debug/parity, level l's candidate labels of one pair as
+ *                     int32 [H_l][W_l][k_l] (ascending per pixel).
+ * ------------------------------------------------------------------------- */
+typedef struct vsbp_csbp vsbp_csbp;
+int csbp_create(int W, int H, int ndisp, int levels, int iters, int k0, float lambda, float data_trunc,
+                float disc_trunc, vsbp_csbp **out);
+size_t csbp_workspace_bytes(const vsbp_csbp *ctx, int batch);
+int csbp_set_workspace(vsbp_csbp *ctx, void *dptr, size_t bytes, int batch);
+int csbp_disparity_batch(vsbp_csbp *ctx, int B, const uint8_t *left, const uint8_t *right, int32_t *disp,
+                         void *stream);
+int csbp_get_candidates(vsbp_csbp *ctx, int pair, int level, int32_t *out, void *stream);
+void csbp_destroy(vsbp_csbp *ctx);
+
+/* ---------------------------------------------------------------------------
  * harris_corners_batch -- row f3, Harris corners on a grid (§2.3 Eq.4-5;
  * P:84 "a 30x30 grid ... Harris corners inside each grid individually"; SPEC
  * S:310-316; R-28, R-29), for n grey images:

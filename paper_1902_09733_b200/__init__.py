@@ -67,6 +67,13 @@ _EXPORTS = {
     "prep_downsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                         C.c_void_p]),
     "prep_downsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "csbp_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
+                              C.c_float, C.c_void_p]),
+    "csbp_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int]),
+    "csbp_set_workspace": (C.c_int, [C.c_void_p, C.c_void_p, C.c_size_t, C.c_int]),
+    "csbp_disparity_batch": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "csbp_get_candidates": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "csbp_destroy": (None, [C.c_void_p]),
     "harris_corners_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int,
                                        C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
     "zssd_match_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int,
@@ -198,6 +205,55 @@ class StereoBP:
         out = torch.empty((h, w, self.L), dtype=torch.int32, device=self.workspace.device)
         _check(lib().bp_get_costs(self._h, pair, level, _dev(out, torch.int32, "out"), _stream(stream)),
                "bp_get_costs")
+        return out
+
+
+class ConstantSpaceBP:
+    """Row f2: constant-space BP, the paper's [4] (R-32..R-35).
+    Level l keeps k_l = min(ndisp, k0 * 2^l) candidate labels per pixel.  Owns its
+    device workspace for up to ``batch`` pairs."""
+
+    def __init__(self, W, H, ndisp, levels, iters, k0, lam=0.07, data_trunc=15.0, disc_trunc=1.7, batch=1,
+                 device="cuda"):
+        self._h = C.c_void_p()
+        _check(lib().csbp_create(W, H, ndisp, levels, iters, k0, lam, data_trunc, disc_trunc, C.byref(self._h)),
+               "csbp_create")
+        self.W, self.H, self.L, self.levels, self.k0, self.batch = W, H, ndisp, levels, k0, batch
+        nbytes = int(lib().csbp_workspace_bytes(self._h, batch))
+        self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
+        _check(lib().csbp_set_workspace(self._h, C.c_void_p(self.workspace.data_ptr()), nbytes, batch),
+               "csbp_set_workspace")
+
+    def __del__(self):
+        h = getattr(self, "_h", None)
+        if h is not None and h.value and _lib is not None:
+            _lib.csbp_destroy(h)
+            self._h = None
+
+    def k(self, level: int) -> int:
+        return min(self.L, self.k0 << level)
+
+    def disparity(self, left: torch.Tensor, right: torch.Tensor, out: torch.Tensor | None = None, stream=None):
+        squeeze = left.dim() == 2
+        if squeeze:
+            left, right = left.unsqueeze(0), right.unsqueeze(0)
+        B = left.shape[0]
+        if tuple(left.shape) != (B, self.H, self.W) or tuple(right.shape) != (B, self.H, self.W):
+            raise ValueError(f"expected [B,{self.H},{self.W}] images")
+        if out is None:
+            out = torch.empty((B, self.H, self.W), dtype=torch.int32, device=left.device)
+        _check(lib().csbp_disparity_batch(self._h, B, _dev(left, torch.uint8, "left"),
+                                          _dev(right, torch.uint8, "right"), _dev(out, torch.int32, "disp"),
+                                          _stream(stream)), "csbp_disparity_batch")
+        return out[0] if squeeze else out
+
+    def candidates(self, pair: int, level: int, stream=None) -> torch.Tensor:
+        w, h = self.W, self.H
+        for _ in range(level):
+            w, h = (w + 1) // 2, (h + 1) // 2
+        out = torch.empty((h, w, self.k(level)), dtype=torch.int32, device=self.workspace.device)
+        _check(lib().csbp_get_candidates(self._h, pair, level, _dev(out, torch.int32, "out"), _stream(stream)),
+               "csbp_get_candidates")
         return out
 
 
@@ -376,7 +432,7 @@ class StereoPipeline:
 
     def __init__(self, W_hi, H_hi, s, ndisp, levels, iters, batch, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
                  sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0,
-                 camera=None, features=None):
+                 camera=None, features=None, csbp_k0=None):
         self.W_hi, self.H_hi, self.s, self.B = W_hi, H_hi, s, batch
         self.W, self.H = W_hi // s, H_hi // s
         self.sigma_s = 15.0 / s if sigma_s is None else sigma_s  # R-16
@@ -384,8 +440,13 @@ class StereoPipeline:
         self.radius = -(-5 // s) if radius is None else radius
         self.min_disp = min_disp
         self.Q = Q
-        self.bp = StereoBP(self.W, self.H, ndisp, levels, iters, lam, data_trunc, disc_trunc, batch=batch,
-                           msg_bytes=msg_bytes, device=device)
+        if csbp_k0:
+            # row f2: the constant-space BP of the paper's [4] in place of the full BP
+            self.bp = ConstantSpaceBP(self.W, self.H, ndisp, levels, iters, csbp_k0, lam, data_trunc, disc_trunc,
+                                      batch=batch, device=device)
+        else:
+            self.bp = StereoBP(self.W, self.H, ndisp, levels, iters, lam, data_trunc, disc_trunc, batch=batch,
+                               msg_bytes=msg_bytes, device=device)
         dev = torch.device(device)
         self.gray = torch.empty((2, batch, self.H, self.W), dtype=torch.uint8, device=dev)
         self.disp = torch.empty((batch, self.H, self.W), dtype=torch.int32, device=dev)

@@ -80,3 +80,25 @@ cudaError_t launch_zssd_match(int n, const uint8_t *img1, const uint8_t *img2, i
                               int ncorner, int r, int sr, int64_t max_cost, int32_t *match, int64_t *mcost,
                               cudaStream_t st);
 }  // namespace vsbp
+
+namespace vsbp {
+// row f2 (csbp.cu): constant-space BP
+constexpr int CS_KMAX = 64;  // candidates per pixel handled by the kernels
+struct CsbpArgs {
+    int W, H, L;             // level-0 (full BP resolution) image and labels
+    int lam_q, tau_d, tau_q, S;
+};
+struct CsbpLevel {
+    int l, W, H, n, k;       // level index, dims, pixels, candidates per pixel
+    uint16_t *cand;          // [B][n][k] ascending labels
+    int32_t *dsel;           // [B][n][k] data cost of each candidate at this level
+    int32_t *msg;            // [B][n][4][k] incoming (receiver-stored) messages
+};
+cudaError_t launch_csbp_top(const uint8_t *left, const uint8_t *right, const CsbpArgs &a, const CsbpLevel &lv, int B,
+                            cudaStream_t st);
+cudaError_t launch_csbp_init(const uint8_t *left, const uint8_t *right, const CsbpArgs &a, const CsbpLevel &lv,
+                             const CsbpLevel &pv, int B, cudaStream_t st);
+cudaError_t launch_csbp_update(const CsbpArgs &a, const CsbpLevel &lv, int colour, int B, cudaStream_t st);
+cudaError_t launch_csbp_wta(const CsbpLevel &lv, int32_t *disp, int B, cudaStream_t st);
+cudaError_t launch_csbp_export(const uint16_t *cand, size_t n, int32_t *out, cudaStream_t st);
+}  // namespace vsbp

@@ -446,3 +446,46 @@ def test_pipeline_features_match_oracle():
     assert np.array_equal(pipe.corners[0].cpu().numpy(), xy_o)
     assert np.array_equal(pipe.matches[0][0].cpu().numpy(), m_o)
     assert np.array_equal(pipe.matches[1][0].cpu().numpy(), c_o)
+
+
+# ----------------------------------------------------------------------------- f2
+def check_csbp(left, right, L, levels, iters, k0, **kw):
+    left, right = np.asarray(left), np.asarray(right)
+    H, W = left.shape
+    cs = P.ConstantSpaceBP(W, H, L, levels, iters, k0, batch=2, device=dev(), **kw)
+    disp = cs.disparity(to_dev(np.stack([left, left])), to_dev(np.stack([right, right]))).cpu().numpy()
+    d_o, cands_o = oracle.csbp_disparity(left, right, L, levels, iters, k0, return_candidates=True, **kw)
+    assert np.array_equal(disp[0], d_o) and np.array_equal(disp[1], d_o)
+    for lv in range(levels):
+        assert np.array_equal(cs.candidates(1, lv).cpu().numpy(), cands_o[lv]), f"candidates of level {lv}"
+    return disp[0]
+
+
+def test_csbp_config1_shift():
+    l, r = synthgen.shifted_pair(1, 64, 48, 5)
+    d = check_csbp(l, r, 16, 3, 5, 2)
+    assert np.mean(d[:, 5:] == 5) >= 0.999
+
+
+@pytest.mark.parametrize("seed", range(16))
+def test_csbp_fuzz(seed):
+    rng = np.random.default_rng(2000 + seed)
+    W = int(rng.choice([1, 2, 3, int(rng.integers(4, 60))]))
+    H = int(rng.choice([1, 2, int(rng.integers(3, 50))]))
+    L = int(rng.choice([2, 5, 16, 24, 64]))
+    levels = int(rng.integers(1, 5))
+    k0 = int(rng.choice([1, 2, 3, 4, 8]))
+    if min(L, k0 << (levels - 1)) > 64:
+        k0 = 1
+    iters = int(rng.integers(1, 8))
+    left = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    right = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    check_csbp(left, right, L, levels, iters, k0)
+
+
+def test_csbp_config2_full_size():
+    """676x380, L=64, 5 levels x 5 iterations, k0=2 (k = 2,4,8,16,32)."""
+    left, right, d_lo = synthgen.stereo_pair_rgb(0)
+    gl, gr = oracle.prep(left, 4), oracle.prep(right, 4)
+    d = check_csbp(gl, gr, 64, 5, 5, 2)
+    assert np.mean(d == d_lo) > 0.8
