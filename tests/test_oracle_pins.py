@@ -634,3 +634,60 @@ def test_csbp_recovers_constant_and_row_plane_shift():
     valid = (np.arange(160)[None, :] >= 40) & ~step[:, None]
     frac = np.mean(disp[valid] == truth[valid])
     assert frac >= 0.99, frac
+
+
+# ----------------------------------------------------------------------------- f4 ICP
+def _rot(axis, deg):
+    a = np.asarray(axis, float) / np.linalg.norm(axis)
+    th = np.deg2rad(deg)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K  # Rodrigues
+
+
+def test_icp_identity_and_constructed_motion():
+    from oracle import icp
+    rng = np.random.default_rng(5)
+    src = rng.uniform(-5, 5, size=(400, 3))
+    r = icp.icp_register(src, src, max_iter=5)
+    assert np.allclose(r["T"], np.hstack([np.eye(3), np.zeros((3, 1))]), atol=1e-12) and r["rms"] <= 1e-12
+    R, t = _rot([1, 2, 3], 5.0), np.array([0.2, -0.1, 0.15])
+    tgt = src @ R.T + t                                                   # 5 deg, 0.2 m
+    r = icp.icp_register(src, tgt, max_iter=60, max_dist=2.0, eps=1e-12)
+    assert np.allclose(r["T"][:, :3], R, atol=1e-6) and np.allclose(r["T"][:, 3], t, atol=1e-6)
+    assert all(b <= a + 1e-12 for a, b in zip(r["rms_history"], r["rms_history"][1:]))  # S:480 monotone
+
+
+def test_icp_rigid_update_is_the_least_squares_motion():
+    """Exact correspondences: the SVD update recovers the motion in one step and is
+    a proper rotation (det +1) -- also for a mirrored-looking planar set."""
+    from oracle import icp
+    rng = np.random.default_rng(6)
+    p = rng.normal(size=(50, 3))
+    R, t = _rot([0, 0, 1], 40.0), np.array([1.0, 2.0, 3.0])
+    T = icp.rigid_update(p, p @ R.T + t)
+    assert np.allclose(T[:, :3], R, atol=1e-12) and np.allclose(T[:, 3], t, atol=1e-12)
+    flat = p.copy()
+    flat[:, 2] = 0.0
+    T = icp.rigid_update(flat, flat @ R.T + t)
+    assert abs(np.linalg.det(T[:, :3]) - 1.0) < 1e-12
+
+
+def test_icp_far_clouds_fail_and_nan_rows_dropped():
+    from oracle import icp
+    rng = np.random.default_rng(7)
+    a = rng.uniform(0, 1, size=(100, 3))
+    r = icp.icp_register(a, a + 100.0, max_dist=0.5)
+    assert r["iters"] == -1                                                # S:476 no pairs
+    b = a.copy()
+    b[::3] = np.nan
+    r1 = icp.icp_register(b, a, max_iter=3)
+    assert r1["n_pairs"][0] == np.sum(~np.isnan(b[:, 0]))
+
+
+def test_icp_nearest_is_brute_force_minimum():
+    from oracle import icp
+    rng = np.random.default_rng(8)
+    P, Q = rng.normal(size=(37, 3)), rng.normal(size=(53, 3))
+    j, d2 = icp.nearest(P, Q, chunk=5)
+    full = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(axis=2)
+    assert np.array_equal(j, full.argmin(axis=1)) and np.allclose(d2, full.min(axis=1), rtol=1e-15)
