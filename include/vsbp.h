@@ -209,6 +209,24 @@ int csbp_get_candidates(vsbp_csbp *ctx, int pair, int level, int32_t *out, void 
 void csbp_destroy(vsbp_csbp *ctx);
 
 /* ---------------------------------------------------------------------------
+ * icp_register -- row f4, point-to-point ICP between two clouds ("CUDA
+ * accelerated Iterative Closest Point (ICP) [6] ... point clouds calculated from
+ * low-resolution disparity maps using Equation 3"; R-36):
+ *   src, tgt : float [n][3] device clouds (rows with a NaN are ignored, R-21)
+ *   init     : HOST double[12], the initial [R|t] (row-major 3x4), e.g. the EPnP
+ *              relative pose; max_iter >= 1, max_dist > 0 (m, pairing radius and
+ *              grid cell), eps > 0 (rms-change stop), stride >= 1 (source subsample)
+ *   ws       : device workspace of icp_workspace_bytes(ns, nt) bytes (256-aligned)
+ *   out      : DEVICE double[16] = {R|t (12), rms, iterations (-1: no pairs),
+ *              converged (0/1), pairs of the last iteration}
+ * Pairing, reductions and the rigid solve run on the device in float64; the
+ * max_iter iterations are enqueued without host synchronisation.
+ * ------------------------------------------------------------------------- */
+size_t icp_workspace_bytes(int ns, int nt);
+int icp_register(const float *src, int ns, const float *tgt, int nt, const double *init, int max_iter,
+                 double max_dist, double eps, int stride, void *ws, size_t ws_bytes, double *out, void *stream);
+
+/* ---------------------------------------------------------------------------
  * harris_corners_batch -- row f3, Harris corners on a grid (§2.3 Eq.4-5;
  * P:84 "a 30x30 grid ... Harris corners inside each grid individually"; SPEC
  * S:310-316; R-28, R-29), for n grey images:

@@ -67,6 +67,9 @@ _EXPORTS = {
     "prep_downsample_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p,
                                         C.c_void_p]),
     "prep_downsample": (C.c_int, [C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
+    "icp_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int]),
+    "icp_register": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_double,
+                               C.c_double, C.c_int, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p]),
     "csbp_create": (C.c_int, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
                               C.c_float, C.c_void_p]),
     "csbp_workspace_bytes": (C.c_size_t, [C.c_void_p, C.c_int]),
@@ -352,6 +355,26 @@ def zssd_match(img1: torch.Tensor, img2: torch.Tensor, xy: torch.Tensor, r: int 
     if squeeze:
         return match[0], cost[0]
     return match, cost
+
+
+def icp_register(src: torch.Tensor, tgt: torch.Tensor, init=None, max_iter: int = 20, max_dist: float = 1.0,
+                 eps: float = 1e-4, stride: int = 1, stream=None) -> torch.Tensor:
+    """Row f4 (R-36): point-to-point ICP of float32 [n,3] clouds on the device.
+    Returns a device float64 [16] tensor {R|t (12), rms, iterations, converged,
+    pairs}; nothing is synchronised."""
+    src = src.reshape(-1, 3)
+    tgt = tgt.reshape(-1, 3)
+    ns, nt = src.shape[0], tgt.shape[0]
+    T0 = np.hstack([np.eye(3), np.zeros((3, 1))]) if init is None else np.asarray(init, np.float64).reshape(3, 4)
+    initd = (C.c_double * 12)(*[float(v) for v in T0.ravel()])
+    nbytes = int(lib().icp_workspace_bytes(ns, nt))
+    ws = torch.empty(nbytes, dtype=torch.uint8, device=src.device)
+    out = torch.empty(16, dtype=torch.float64, device=src.device)
+    _check(lib().icp_register(_dev(src, torch.float32, "src"), ns, _dev(tgt, torch.float32, "tgt"), nt, initd,
+                              max_iter, float(max_dist), float(eps), stride, C.c_void_p(ws.data_ptr()), nbytes,
+                              _dev(out, torch.float64, "out"), _stream(stream)), "icp_register")
+    out._workspace = ws  # keep the workspace alive until the caller is done with `out`
+    return out
 
 
 def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.ndarray:

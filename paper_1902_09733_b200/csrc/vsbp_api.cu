@@ -578,6 +578,20 @@ int zssd_match_batch(int n, const uint8_t *img1, const uint8_t *img2, int W, int
     return VSBP_OK;
 }
 
+size_t icp_workspace_bytes(int ns, int nt) { return (ns < 1 || nt < 1) ? 0 : vsbp::icp_workspace_bytes(ns, nt); }
+
+int icp_register(const float *src, int ns, const float *tgt, int nt, const double *init, int max_iter,
+                 double max_dist, double eps, int stride, void *ws, size_t ws_bytes, double *out, void *stream)
+{
+    if (!src || !tgt || !init || !ws || !out || ns < 1 || nt < 1 || max_iter < 1 || max_iter > 10000 || stride < 1)
+        return VSBP_EINVAL;
+    if (!(max_dist > 0.0) || !(eps > 0.0) || ((uintptr_t)ws & 255)) return VSBP_EINVAL;
+    if (ns > (1 << 28) || nt > (1 << 28)) return VSBP_EINVAL;
+    if (ws_bytes < vsbp::icp_workspace_bytes(ns, nt)) return VSBP_EDIM;
+    CK(vsbp::launch_icp(src, ns, tgt, nt, init, max_iter, max_dist, eps, stride, ws, out, (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
 int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsigned long long *n_valid,
                        uint64_t first_pair_id, vsbp_summary *summary, void *stream)
 {

@@ -102,3 +102,10 @@ cudaError_t launch_csbp_update(const CsbpArgs &a, const CsbpLevel &lv, int colou
 cudaError_t launch_csbp_wta(const CsbpLevel &lv, int32_t *disp, int B, cudaStream_t st);
 cudaError_t launch_csbp_export(const uint16_t *cand, size_t n, int32_t *out, cudaStream_t st);
 }  // namespace vsbp
+
+namespace vsbp {
+// row f4 (icp.cu): point-to-point ICP in float64
+size_t icp_workspace_bytes(int ns, int nt);
+cudaError_t launch_icp(const float *src, int ns, const float *tgt, int nt, const double init[12], int max_iter,
+                       double max_dist, double eps, int stride, void *ws, double *out, cudaStream_t st);
+}  // namespace vsbp

@@ -489,3 +489,61 @@ def test_csbp_config2_full_size():
     gl, gr = oracle.prep(left, 4), oracle.prep(right, 4)
     d = check_csbp(gl, gr, 64, 5, 5, 2)
     assert np.mean(d == d_lo) > 0.8
+
+
+# ----------------------------------------------------------------------------- f4
+def _rot(axis, deg):
+    a = np.asarray(axis, float) / np.linalg.norm(axis)
+    th = np.deg2rad(deg)
+    K = np.array([[0, -a[2], a[1]], [a[2], 0, -a[0]], [-a[1], a[0], 0]])
+    return np.eye(3) + np.sin(th) * K + (1 - np.cos(th)) * K @ K
+
+
+def _icp_both(src, tgt, **kw):
+    from oracle import icp
+    src = np.ascontiguousarray(src, np.float32)
+    tgt = np.ascontiguousarray(tgt, np.float32)
+    o = icp.icp_register(src.astype(np.float64), tgt.astype(np.float64), **kw)
+    g = P.icp_register(to_dev(src), to_dev(tgt), **kw).cpu().numpy()
+    return o, g
+
+
+@pytest.mark.parametrize("deg,shift,stride", [(5.0, 0.2, 1), (2.0, 0.5, 3), (0.0, 0.0, 1)])
+def test_icp_constructed_motion_matches_oracle(deg, shift, stride):
+    rng = np.random.default_rng(int(deg * 10) + stride)
+    src = rng.uniform(-8, 8, size=(3000, 3)).astype(np.float32)
+    src[::17] = np.nan                                   # invalid points are dropped (R-21)
+    R, t = _rot([1, -2, 0.5], deg), np.array([shift, -shift / 2, shift / 3])
+    tgt = (src.astype(np.float64) @ R.T + t).astype(np.float32)
+    o, g = _icp_both(src, tgt, max_iter=40, max_dist=1.0, eps=1e-9, stride=stride)
+    assert int(g[13]) == o["iters"] and bool(g[14]) == o["converged"]
+    assert int(g[15]) == o["n_pairs"][-1]
+    assert np.max(np.abs(g[:12].reshape(3, 4) - o["T"])) <= 1e-9
+    assert abs(g[12] - o["rms"]) <= 1e-9
+
+
+def test_icp_on_low_res_eq3_clouds():
+    """Clouds of Eq.3 at BP resolution (the paper's ICP input): a pair's cloud
+    against itself moved by a small rigid motion."""
+    left, right, _ = synthgen.stereo_pair_rgb(3)
+    gl, gr = oracle.prep(left, 4), oracle.prep(right, 4)
+    d = oracle.bp_disparity(gl, gr, 64, 5, 5)
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"] / 4, I["f_dv"] / 4, (I["u0"] + 0.5) / 4 - 0.5, (I["v0"] + 0.5) / 4 - 0.5, I["B"])
+    xyz, _ = oracle.reproject(d.astype(np.float64), Q, 1.0)
+    src = xyz.reshape(-1, 3).astype(np.float32)
+    R, t = _rot([0, 0, 1], 1.0), np.array([0.3, 0.1, -0.2])
+    tgt = (src.astype(np.float64) @ R.T + t).astype(np.float32)
+    o, g = _icp_both(src, tgt, max_iter=30, max_dist=2.0, eps=1e-7, stride=4)
+    assert int(g[13]) == o["iters"] and int(g[15]) == o["n_pairs"][-1]
+    assert np.max(np.abs(g[:12].reshape(3, 4) - o["T"])) <= 1e-8
+
+
+def test_icp_failure_and_identity():
+    rng = np.random.default_rng(1)
+    a = rng.uniform(0, 1, size=(200, 3)).astype(np.float32)
+    o, g = _icp_both(a, a + 100.0, max_iter=5, max_dist=0.5)
+    assert o["iters"] == -1 and int(g[13]) == -1
+    o, g = _icp_both(a, a, max_iter=5, max_dist=0.5)
+    assert np.max(np.abs(g[:12].reshape(3, 4) - np.hstack([np.eye(3), np.zeros((3, 1))]))) <= 1e-12
+    assert int(g[13]) == o["iters"]
