@@ -90,7 +90,7 @@ __device__ __forceinline__ uint32_t chunk_min(const uint32_t h[8])
 // PAD: some labels of the chunk are >= L.  WTA: write the WTA label of the pixel.
 // SIGNED: beliefs < 2^15, normalise+clamp in one signed VIADDMNMX.
 template <typename TD, int MODE, bool PAD, bool WTA, bool SIGNED>
-__global__ void __launch_bounds__(256) k_update_fast(FastArgs a, const TD *__restrict__ D)
+__global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__restrict__ D)
 {
     const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
     const int b = blockIdx.y;
