@@ -244,7 +244,7 @@ template <> struct GuideVec<2> {  // 6 bytes, 2-byte aligned
 };
 
 template <int R, int S, int NR>
-__global__ void __launch_bounds__(JB_X * JB_Y / NR) k_jbu_vec(const int32_t *__restrict__ disp_lo,
+__global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? 5 : 3) k_jbu_vec(const int32_t *__restrict__ disp_lo,
                                                            const uint8_t *__restrict__ guide,
                                                            float *__restrict__ disp_hi, float *__restrict__ xyz,
                                                            unsigned long long *__restrict__ n_valid,

@@ -1,0 +1,103 @@
+#!/usr/bin/env python
+"""Per-row device timings of the widened rows (f1-f4) on one B200, CUDA events on
+the launching stream after warm-up.  bench.py remains the contract benchmark (the
+a0-a8 path); this script measures the "next" rows at their natural units.
+
+  python tools/bench_rows.py [--out profiles/r01_rows.json]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+import torch  # noqa: E402
+
+import paper_1902_09733_b200 as P  # noqa: E402
+import synthgen  # noqa: E402
+
+
+def timed(fn, reps=10, warm=3):
+    for _ in range(warm):
+        fn()
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        fn()
+    e1.record()
+    torch.cuda.synchronize()
+    return e0.elapsed_time(e1) / reps
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--out", default=None)
+    ap.add_argument("--batch", type=int, default=16)
+    a = ap.parse_args()
+    dev = torch.device("cuda:0")
+    B = a.batch
+    res = {"gpu": torch.cuda.get_device_name(0), "batch": B}
+    left, right, _ = synthgen.stereo_pair_rgb(0)
+    L = torch.from_numpy(np.stack([left] * B)).to(dev)
+    R = torch.from_numpy(np.stack([right] * B)).to(dev)
+
+    # f1: undistortion + grey/box downsample of B raw 2.7K frames (left: with the rectified guide)
+    cam = (1400.0, 1400.0, 1351.5, 759.5, -0.25, 0.08, -0.01)
+    rect = torch.empty_like(L)
+    gray = torch.empty((B, 380, 676), dtype=torch.uint8, device=dev)
+    ms = timed(lambda: P.rectify_prep(L, cam, 4, gray=gray, rect=rect))
+    res["f1_rectify_prep_with_rgb_out"] = {"ms_per_frame": ms / B, "GB_per_s": B * 2 * 2704 * 1520 * 3 / (ms / 1e3) / 1e9}
+    ms = timed(lambda: P.rectify_prep(L, cam, 4, gray=gray))
+    res["f1_rectify_prep_grey_only"] = {"ms_per_frame": ms / B}
+
+    # grey pairs for BP / features
+    gl = P.prep_downsample(L, 4)
+    gr = P.prep_downsample(R, 4)
+
+    # full BP (a1-a5) for reference, then f2 constant-space BP
+    bp = P.StereoBP(676, 380, 64, 5, 5, batch=B, device=dev)
+    out = torch.empty((B, 380, 676), dtype=torch.int32, device=dev)
+    res["a1_a5_full_bp"] = {"ms_per_pair": timed(lambda: bp.disparity(gl, gr, out=out)) / B}
+    for k0 in (1, 2, 4):
+        cs = P.ConstantSpaceBP(676, 380, 64, 5, 5, k0, batch=B, device=dev)
+        res[f"f2_csbp_k0_{k0}"] = {"ms_per_pair": timed(lambda: cs.disparity(gl, gr, out=out)) / B,
+                                  "workspace_MB_per_pair": cs.workspace.numel() / B / 1e6}
+    res["a1_a5_full_bp"]["workspace_MB_per_pair"] = bp.workspace.numel() / B / 1e6
+
+    # f3: Harris corners on the 30x30 grid + ZSSD matching into the right frame
+    for sr in (16, 48):
+        def feat():
+            _, xy, _, _ = P.harris_corners(gl, 30, 30, 4, 10 ** 9)
+            P.zssd_match(gl, gr, xy, 5, sr)
+        res[f"f3_harris_zssd_sr{sr}"] = {"ms_per_pair": timed(feat) / B}
+    res["f3_harris_only"] = {"ms_per_pair": timed(lambda: P.harris_corners(gl, 30, 30, 4, 10 ** 9)) / B}
+
+    # f4: ICP of a low-res Eq.3 cloud against itself moved by a small rigid motion
+    import oracle  # test infrastructure: only to build the input cloud (Eq.3 in double)
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"] / 4, I["f_dv"] / 4, (I["u0"] + 0.5) / 4 - 0.5, (I["v0"] + 0.5) / 4 - 0.5, I["B"])
+    d = out[0].cpu().numpy().astype(np.float64)
+    xyz, _ = oracle.reproject(d, Q, 1.0)
+    src = xyz.reshape(-1, 3).astype(np.float32)
+    th = np.deg2rad(1.0)
+    Rm = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]])
+    tgt = (src.astype(np.float64) @ Rm.T + [0.3, 0.1, -0.2]).astype(np.float32)
+    S, T = torch.from_numpy(src).to(dev), torch.from_numpy(tgt).to(dev)
+    ms = timed(lambda: P.icp_register(S, T, max_iter=20, max_dist=2.0, eps=1e-7, stride=4), reps=5)
+    o = P.icp_register(S, T, max_iter=20, max_dist=2.0, eps=1e-7, stride=4).cpu().numpy()
+    res["f4_icp_lowres_cloud"] = {"ms_per_registration": ms, "points": int(np.sum(~np.isnan(src[:, 0]))),
+                                  "stride": 4, "iterations": int(o[13]), "pairs": int(o[15]), "rms_m": float(o[12])}
+    print(json.dumps(res, indent=1))
+    if a.out:
+        with open(a.out, "w") as f:
+            json.dump(res, f, indent=1)
+
+
+if __name__ == "__main__":
+    main()
