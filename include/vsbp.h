@@ -75,6 +75,13 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        (same results, bit for bit). */
 #define VSBP_OPT_MSG_BYTES 1
 #define VSBP_OPT_KERNEL 2
+/*   VSBP_OPT_DIMG      : 1 = the packed kernel computes the level-0 data term from
+ *                        the grey images inside the message update, so D_0 is
+ *                        neither stored nor read (bp_get_costs rebuilds it on demand
+ *                        from the last call's images); 0 (default) = store and read
+ *                        D_0.  Results are identical; 1 trades 11 % of the level-0
+ *                        bytes for ~10 % more ALU work and measured slower. */
+#define VSBP_OPT_DIMG 3
 int bp_set_option(vsbp_bp *ctx, int option, int value);
 
 /* Quantised parameters: out[0..7] = {lambda_q, tau_d, tau_q, S, msg_bytes,

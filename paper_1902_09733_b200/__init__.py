@@ -29,6 +29,7 @@ LIB_PATH = os.path.join(_HERE, "libvsbp.so")
 
 VSBP_OPT_MSG_BYTES = 1
 VSBP_OPT_KERNEL = 2
+VSBP_OPT_DIMG = 3
 _ERRNAMES = {-1: "VSBP_EINVAL", -2: "VSBP_EDIM", -3: "VSBP_EOVERFLOW", -4: "VSBP_ECUDA"}
 
 
@@ -138,7 +139,7 @@ class StereoBP:
     device workspace (a torch uint8 tensor) for up to ``batch`` pairs."""
 
     def __init__(self, W, H, ndisp, levels, iters, lam=0.07, data_trunc=15.0, disc_trunc=1.7, batch=1,
-                 msg_bytes=0, kernel=0, device="cuda"):
+                 msg_bytes=0, kernel=0, device="cuda", dimg=0):
         self._h = C.c_void_p()
         _check(lib().bp_create(W, H, ndisp, levels, iters, lam, data_trunc, disc_trunc, C.byref(self._h)),
                "bp_create")
@@ -146,6 +147,8 @@ class StereoBP:
             _check(lib().bp_set_option(self._h, VSBP_OPT_MSG_BYTES, msg_bytes), "bp_set_option")
         if kernel:
             _check(lib().bp_set_option(self._h, VSBP_OPT_KERNEL, kernel), "bp_set_option")
+        if dimg:
+            _check(lib().bp_set_option(self._h, VSBP_OPT_DIMG, 1), "bp_set_option")
         self.W, self.H, self.L, self.levels, self.iters, self.batch = W, H, ndisp, levels, iters, batch
         nbytes = int(lib().bp_workspace_bytes(self._h, batch))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)
@@ -182,6 +185,7 @@ class StereoBP:
         _check(lib().bp_disparity_batch(self._h, B, _dev(left, torch.uint8, "left"),
                                         _dev(right, torch.uint8, "right"), _dev(out, torch.int32, "disp"),
                                         _stream(stream)), "bp_disparity_batch")
+        self._last_inputs = (left, right)  # costs(0) may rebuild D_0 from them (VSBP_OPT_DIMG)
         return out[0] if squeeze else out
 
     def messages(self, pair: int, level: int, stream=None) -> torch.Tensor:

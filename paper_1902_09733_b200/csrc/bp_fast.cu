@@ -26,6 +26,8 @@
 // there (its belief D + sum of 4 incoming is in registers); MODE 3 computes only
 // the WTA (no messages) for the other colour.  HBM traffic per updated pixel:
 // L*w_D + 8L bytes (MODE 3: L*w_D + 4L).
+#include <type_traits>
+
 #include "vsbp_internal.cuh"
 #include "vsbp_kernels.h"
 
@@ -75,6 +77,58 @@ template <> struct DLoad<uint16_t> {
         r[4] = b.x, r[5] = b.y, r[6] = b.z, r[7] = b.w;
     }
 };
+
+// level-0 data term computed from the grey images instead of read from D_0 (the
+// TD = ImgD instantiation): R-2 / R-8, D(x,y,d) = lambda_q * min(|L(x,y) - R(x-d,y)|,
+// tau_d) or lambda_q * tau_d for x - d < 0.  The 16 right-image bytes R(x-d0-15 ..
+// x-d0) come in as four funnel-aligned words; VABSDIFF4 gives four |L - R| per
+// instruction, byte pairs (d0+j, d0+j+8) are gathered into u16x2 with PRMT, then
+// min(., tau_d) (VIMNMX.U16x2) and one packed IMAD by lambda_q.  Per updated pixel
+// this replaces L bytes of D_0 traffic by ~2 bytes of (L1-resident) image.
+struct ImgD {};
+
+__device__ __forceinline__ void dimg_load(const FastArgs &a, int b, int x, int y, int d0, uint32_t dv[8])
+{
+    const size_t row = ((size_t)b * a.H + y) * (size_t)a.W;
+    const int l = __ldg(a.gl + row + x);
+    const int a0 = x - d0 - 15;  // first right-image column needed
+    if (a0 >= 0 && row + (size_t)a0 + 20 <= a.img_elems) {
+        const uintptr_t pa = (uintptr_t)(a.gr + row + a0);
+        const uint32_t *wp = reinterpret_cast<const uint32_t *>(pa & ~(uintptr_t)3);
+        const uint32_t sh = (uint32_t)(pa & 3) * 8u;
+        const uint32_t w0 = __ldg(wp), w1 = __ldg(wp + 1), w2 = __ldg(wp + 2), w3 = __ldg(wp + 3);
+        const uint32_t w4 = sh ? __ldg(wp + 4) : 0u;
+        const uint32_t l4 = (uint32_t)l * 0x01010101u;
+        // D_k byte c = |L - R(a0 + 4k + c)| = label d0 + 15 - 4k - c
+        const uint32_t D0 = __vabsdiffu4(l4, __funnelshift_r(w0, w1, sh));
+        const uint32_t D1 = __vabsdiffu4(l4, __funnelshift_r(w1, w2, sh));
+        const uint32_t D2 = __vabsdiffu4(l4, __funnelshift_r(w2, w3, sh));
+        const uint32_t D3 = __vabsdiffu4(l4, __funnelshift_r(w3, w4, sh));
+        const uint32_t E0 = D0 & 0x00FF00FFu, O0 = (D0 >> 8) & 0x00FF00FFu;
+        const uint32_t E1 = D1 & 0x00FF00FFu, O1 = (D1 >> 8) & 0x00FF00FFu;
+        const uint32_t E2 = D2 & 0x00FF00FFu, O2 = (D2 >> 8) & 0x00FF00FFu;
+        const uint32_t E3 = D3 & 0x00FF00FFu, O3 = (D3 >> 8) & 0x00FF00FFu;
+        const uint32_t pr[8] = {prmt(O3, O1, 0x7632), prmt(E3, E1, 0x7632), prmt(O3, O1, 0x5410),
+                                prmt(E3, E1, 0x5410), prmt(O2, O0, 0x7632), prmt(E2, E0, 0x7632),
+                                prmt(O2, O0, 0x5410), prmt(E2, E0, 0x5410)};
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dv[j] = __vminu2(pr[j], a.T2d) * a.lam;
+    } else {
+        // left image border (x - d < 0 -> lambda_q * tau_d) or the buffer's last bytes
+        const uint32_t border = a.lam * (a.T2d & 0xFFFFu);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            uint32_t c[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int d = d0 + j + 8 * h, xr = x - d;
+                c[h] = xr >= 0 ? a.lam * (uint32_t)min(abs(l - (int)__ldg(a.gr + row + xr)), (int)(a.T2d & 0xFFFFu))
+                               : border;
+            }
+            dv[j] = c[0] | (c[1] << 16);
+        }
+    }
+}
 
 // min over the 16 labels of a chunk (both halves), replicated in both halves
 __device__ __forceinline__ uint32_t chunk_min(const uint32_t h[8])
@@ -141,7 +195,10 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
     }
     uint32_t dv[8];
     if (io) {
-        DLoad<TD>::load(D + (size_t)b * a.pairD + a.colour * P + r, dv);
+        if constexpr (std::is_same<TD, ImgD>::value)
+            dimg_load(a, b, x, (int)y, d0, dv);
+        else
+            DLoad<TD>::load(D + (size_t)b * a.pairD + a.colour * P + r, dv);
     } else {
 #pragma unroll
         for (int j = 0; j < 8; ++j) dv[j] = 0u;
@@ -250,7 +307,9 @@ cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int
         else VSBP_K(TD_, 3, false, true, false);      \
         break;                                        \
     }
-    if (dbytes == 1) {
+    if (dbytes == 0) {
+        VSBP_M(ImgD)
+    } else if (dbytes == 1) {
         VSBP_M(uint8_t)
     } else {
         VSBP_M(uint16_t)

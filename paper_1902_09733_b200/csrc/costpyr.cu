@@ -133,7 +133,7 @@ __global__ void __launch_bounds__(256) k_costpyr(const uint8_t *__restrict__ lef
                     v[j] = c;
                     acc[j] += c;
                 }
-                store_chunk(a.D[0], a.dbytes[0],
+                if (a.write0) store_chunk(a.D[0], a.dbytes[0],
                             (size_t)b * a.pairD[0] + d_off(0, (x + y) & 1, y, x >> 1, H, a.Wc[0], Lp) + k * CH, v);
             }
         if (a.F > 1) {
@@ -263,7 +263,7 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
                     if (PAD) r[j] &= mask[j];
                     acc[j] += r[j];
                 }
-                store_pairs(a.D[0], a.dbytes[0],
+                if (a.write0) store_pairs(a.D[0], a.dbytes[0],
                             (size_t)b * a.pairD[0] + d_off(0, (x + y) & 1, y, x >> 1, H, a.Wc[0], Lp) + k * CH, r);
             }
         }

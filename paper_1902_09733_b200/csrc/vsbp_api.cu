@@ -16,6 +16,7 @@ struct vsbp_bp {
     int lam_q, tau_d, tau_q, S;
     int Lp, nch, G, log2G;
     int msg_bytes_opt, msg_bytes, kernel;
+    int dimg;  // level-0 data term computed from the images inside the update (no D_0 traffic)
     int Wl[16], Hl[16], Wcl[16];
     int dbytes[16];
     // workspace plan (bytes) for ws_batch pairs
@@ -24,6 +25,7 @@ struct vsbp_bp {
     size_t ws_bytes;
     int ws_batch;
     int last_B;
+    const uint8_t *last_left, *last_right;  // the last call's images (debug cost export)
     // live timing of the a4 launches (bp_timing_enable)
     int timing;
     int n_pending;
@@ -110,6 +112,9 @@ bool use_fast(const vsbp_bp *c, int l)
     return dmax + 4LL * c->tau_q < 65536LL;
 }
 
+// level 0 of the packed kernel computes its data term from the grey images
+bool use_dimg(const vsbp_bp *c) { return c->dimg && use_fast(c, 0) && c->dbytes[0] == 1 && c->tau_d <= 255; }
+
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
 bool fast_signed(const vsbp_bp *c, int l)
 {
@@ -147,6 +152,10 @@ vsbp::FastArgs fast_args(const vsbp_bp *c, int l, char *ws, int32_t *disp)
     a.pairM = (size_t)8 * a.plane;
     a.pairMp = (size_t)8 * a.planep;
     a.SS = (uint32_t)c->S | ((uint32_t)c->S << 16);
+    a.gl = a.gr = nullptr;
+    a.img_elems = 0;
+    a.lam = (uint32_t)c->lam_q;
+    a.T2d = (uint32_t)c->tau_d | ((uint32_t)c->tau_d << 16);
     a.TT = (uint32_t)c->tau_q | ((uint32_t)c->tau_q << 16);
     return a;
 }
@@ -231,6 +240,7 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
         h = (h + 1) / 2;
     }
     c->msg_bytes = bytes_for_max(c->tau_q);
+    c->dimg = 0;  // measured slower (ALU-bound): DESIGN.md §12
     *out = c;
     return VSBP_OK;
 }
@@ -251,6 +261,11 @@ int bp_set_option(vsbp_bp *c, int option, int value)
     if (option == VSBP_OPT_KERNEL) {
         if (value < 0 || value > 1) return VSBP_EINVAL;
         c->kernel = value;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_DIMG) {
+        if (value < 0 || value > 1) return VSBP_EINVAL;
+        c->dimg = value;
         return VSBP_OK;
     }
     return VSBP_EINVAL;
@@ -333,6 +348,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         a.F = F;
         a.lam_q = c->lam_q;
         a.tau_d = c->tau_d;
+        a.write0 = use_dimg(c) ? 0 : 1;  // D_0 is never read when the update computes it
         CK(vsbp::launch_costpyr(left, right, a, B, st));
         l_from = F - 1;
     } else {
@@ -370,7 +386,14 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 vsbp::FastArgs fa = fast_args(c, l, ws, disp);
                 fa.colour = (uint32_t)(t & 1);
                 const bool wta = (l == 0 && t == c->iters - 1);  // a5 fused for this colour
-                CK(vsbp::launch_update_fast(D, c->dbytes[l], fa, B, mode, wta, fast_signed(c, l), st));
+                int db = c->dbytes[l];
+                if (l == 0 && use_dimg(c)) {  // data term from the images, no D_0 read
+                    db = 0;
+                    fa.gl = left;
+                    fa.gr = right;
+                    fa.img_elems = (size_t)B * c->W * c->H;
+                }
+                CK(vsbp::launch_update_fast(D, db, fa, B, mode, wta, fast_signed(c, l), st));
             } else {
                 CK(vsbp::launch_update(D, c->dbytes[l], M, Mp, c->msg_bytes, g, mode, t & 1, c->S, c->tau_q, st));
             }
@@ -391,13 +414,22 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         if (use_fast(c, 0)) {
             vsbp::FastArgs fa = fast_args(c, 0, ws, disp);
             fa.colour = (uint32_t)(((c->iters - 1) & 1) ^ 1);  // the colour not updated last
-            CK(vsbp::launch_update_fast(ws + c->d_off[0], c->dbytes[0], fa, B, 3, true, false, st));
+            int db = c->dbytes[0];
+            if (use_dimg(c)) {
+                db = 0;
+                fa.gl = left;
+                fa.gr = right;
+                fa.img_elems = (size_t)B * c->W * c->H;
+            }
+            CK(vsbp::launch_update_fast(ws + c->d_off[0], db, fa, B, 3, true, false, st));
         } else {
             vsbp::Geom g = geom(c, B, 0);
             CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, -1, st));
         }
     }
     c->last_B = B;
+    c->last_left = left;
+    c->last_right = right;
     return VSBP_OK;
 }
 
@@ -422,6 +454,14 @@ int bp_get_costs(vsbp_bp *c, int pair, int level, int32_t *out, void *stream)
     if (!c->ws || pair >= c->ws_batch) return VSBP_EDIM;
     plan(c, c->ws_batch);
     vsbp::Geom g = geom(c, c->ws_batch, level);
+    if (level == 0 && use_dimg(c)) {
+        // D_0 is not stored on this path (the update computes it): rebuild it from the
+        // last call's images (debug/parity only; needs them still alive)
+        if (!c->last_left || !c->last_right) return VSBP_EINVAL;
+        vsbp::Geom g1 = geom(c, c->last_B, 0);
+        CK(vsbp::launch_costvol(c->last_left, c->last_right, wsp(c) + c->d_off[0], c->dbytes[0], g1, c->lam_q,
+                                c->tau_d, (cudaStream_t)stream));
+    }
     CK(vsbp::launch_export_costs(wsp(c) + c->d_off[level], c->dbytes[level], g, pair, out, (cudaStream_t)stream));
     return VSBP_OK;
 }

@@ -24,6 +24,7 @@ struct CostPyrArgs {
     size_t pairD[5];  // elements per pair of level l's cost array
     int L, Lp, nch, F;
     int lam_q, tau_d;
+    int write0;       // write level 0 (0: only the coarser levels are stored)
     int img_smem;     // set by the launcher
 };
 size_t costpyr_smem(int L, int Lp, int F);
@@ -47,7 +48,12 @@ struct FastArgs {
     uint32_t plane, planep;  // H*Wc*Lp, Hp*Wcp*Lp
     size_t pairD, pairM, pairMp;
     uint32_t SS, TT;         // S and tau_q replicated in both 16-bit halves
+    // level 0 with dbytes == 0: the data term is computed from the grey images
+    const uint8_t *gl, *gr;  // [B][H][W]
+    size_t img_elems;        // B*H*W (bounds of the vector loads)
+    uint32_t lam, T2d;       // lambda_q; tau_d in both 16-bit halves
 };
+// dbytes 1 / 2: D is u8 / u16; dbytes 0: level 0 computed from a.gl / a.gr (ImgD)
 cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
                                cudaStream_t st);
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);

@@ -100,6 +100,24 @@ def test_wide_tau_q_u16_and_i32_storage():
     check_bp_case(l, r, 24, 2, 3, lam=2.0, dt=60.0, st=1000.0)    # tau_q = 128000 -> i32
 
 
+@pytest.mark.parametrize("dimg", [0, 1])
+@pytest.mark.parametrize("W,H,L,levels", [(13, 5, 16, 1), (64, 40, 64, 5), (33, 7, 48, 3)])
+def test_level0_data_term_from_images_or_memory(W, H, L, levels, dimg):
+    """VSBP_OPT_DIMG: the level-0 data term computed inside the update from the
+    images (incl. the left border and the buffer's last bytes) equals reading D_0."""
+    rng = np.random.default_rng(W + 3 * L + dimg)
+    l = rng.integers(0, 256, size=(3, H, W), dtype=np.uint8)
+    r = rng.integers(0, 256, size=(3, H, W), dtype=np.uint8)
+    bp = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg)
+    disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+    for b in range(3):
+        d_o, msgs_o = oracle.bp_disparity(l[b], r[b], L, levels, 5, return_messages=True)
+        assert np.array_equal(disp[b], d_o)
+        assert np.array_equal(bp.messages(b, 0).cpu().numpy(), msgs_o[0])
+    D = oracle.cost_volume(l[2], r[2], L, oracle.quantize(0.07, 15.0, 1.7))
+    assert np.array_equal(bp.costs(2, 0).cpu().numpy(), D)
+
+
 @pytest.mark.parametrize("W,H,L,levels", [(97, 61, 32, 4), (70, 41, 130, 6), (9, 17, 64, 5)])
 def test_generic_and_fused_kernels_agree_with_oracle(W, H, L, levels):
     """VSBP_OPT_KERNEL=1 (separate cost-volume, pyramid and generic update kernels)
