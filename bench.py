@@ -321,6 +321,7 @@ def run_ours(args):
         barrier()
         ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": pairs / (ems / 1000.0), "unit": "pairs/s",
+               "h2d_gbs_per_gpu": args.steps * (left_h.numel() + right_h.numel()) / (ems / 1000.0) / 1e9,
                "h2d_bytes_per_step": int(left_h.numel() + right_h.numel()),
                "d2h_bytes_per_step": int(runner.summary_host.numel() * 8),
                "overlap": "H2D of batch i+1 on a copy stream during compute of batch i"}

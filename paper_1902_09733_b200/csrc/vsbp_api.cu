@@ -3,6 +3,7 @@
 // stacks).  Host code only; every device step is a kernel in bp_kernels.cu or
 // pipeline_kernels.cu.
 #include <cmath>
+#include <cstdlib>
 #include <cstdio>
 #include <cstring>
 #include <new>
@@ -330,7 +331,13 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
     // a1: cost volume, a2: pyramid -- fused for the first F levels when the
     // tile's shared memory fits (costpyr.cu), the rest level by level
     int l_from = 0;
-    const int F = c->levels < 5 ? c->levels : 5;
+    // levels fused into the cost-volume kernel (tuning knob VSBP_COSTPYR_LEVELS, 1..5)
+    static const int fmax = [] {
+        const char *e = getenv("VSBP_COSTPYR_LEVELS");
+        const int v = e ? atoi(e) : 2;  // measured: 2 fused levels best
+        return v < 1 ? 1 : (v > 5 ? 5 : v);
+    }();
+    const int F = c->levels < fmax ? c->levels : fmax;
     if (c->kernel == 0 && vsbp::costpyr_smem(c->L, c->Lp, F) <= 160 * 1024) {
         vsbp::CostPyrArgs a;
         memset(&a, 0, sizeof a);
