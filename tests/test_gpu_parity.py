@@ -565,3 +565,40 @@ def test_icp_failure_and_identity():
     o, g = _icp_both(a, a, max_iter=5, max_dist=0.5)
     assert np.max(np.abs(g[:12].reshape(3, 4) - np.hstack([np.eye(3), np.zeros((3, 1))]))) <= 1e-12
     assert int(g[13]) == o["iters"]
+
+
+# ----------------------------------------------------------------------------- bench configuration
+def test_bench_launch_configuration_sampled_pairs():
+    """The configuration bench.py times (C5: 32 pairs per launch, 2.7K RGB, s=4,
+    L=64, 5x5, JBU r=2): two sampled pairs of the batch (first and last, different
+    scenes) through the whole path against the oracle."""
+    import bench
+    B = 32
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    pipe = P.StereoPipeline(bench.W_HI, bench.H_HI, bench.S_DOWN, bench.NDISP, bench.LEVELS, bench.ITERS, batch=B,
+                            Q=Q, device=dev())
+    lp, rp = bench.make_pool(7000, 2)
+    idx = [0] * (B - 1) + [1]
+    summ = pipe.run(to_dev(lp[idx]), to_dev(rp[idx]), first_pair_id=5).cpu().numpy()
+    Qo = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    for b, k in ((0, 0), (B - 1, 1)):
+        disp_o, hi_o, _, n_o = oracle.pipeline_pair(lp[k], rp[k], bench.S_DOWN, bench.NDISP, bench.LEVELS,
+                                                    bench.ITERS, Qo)
+        assert np.array_equal(pipe.disp[b].cpu().numpy(), disp_o)
+        assert np.max(np.abs(pipe.disp_hi[b].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
+        amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
+        assert abs(int(summ[b, 0]) - n_o) <= amb and int(summ[b, 3]) == 5 + b
+
+
+def test_config4_pipeline_jbu_s2_r3():
+    """C4 with its upsampling (1352x760, L=128, 6 levels x 8 iterations, JBU s=2 r=3)."""
+    left, right, _ = synthgen.stereo_pair_rgb(1, s=2, dmin=16, dmax=96)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    pipe = P.StereoPipeline(2704, 1520, 2, 128, 6, 8, batch=1, Q=Q, device=dev())
+    pipe.run(to_dev(left[None]), to_dev(right[None]))
+    Qo = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    disp_o, hi_o, _, _ = oracle.pipeline_pair(left, right, 2, 128, 6, 8, Qo)
+    assert np.array_equal(pipe.disp[0].cpu().numpy(), disp_o)
+    assert np.max(np.abs(pipe.disp_hi[0].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
