@@ -337,7 +337,7 @@ def run_ours(args):
         all_bytes = sum(x["bytes"] for x in lv)
         all_ms = sum(x["ms"] for x in lv)
         roofline = {
-            "kernel": "k_update (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "kernel": "k_update_fast (a4 message update), level 0", "bound": "hbm", "achieved": achieved, "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(B),
             "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
