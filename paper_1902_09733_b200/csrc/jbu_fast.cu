@@ -243,15 +243,15 @@ template <> struct GuideVec<2> {  // 6 bytes, 2-byte aligned
     }
 };
 
-template <int R, int S, int NR>
-__global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? 5 : 3) k_jbu_vec(const int32_t *__restrict__ disp_lo,
+template <int R, int S, int NR, int P>
+__global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? 5 : 8) : (P == 4 ? 3 : 4)) k_jbu_vec(const int32_t *__restrict__ disp_lo,
                                                            const uint8_t *__restrict__ guide,
                                                            float *__restrict__ disp_hi, float *__restrict__ xyz,
                                                            unsigned long long *__restrict__ n_valid,
                                                            const __grid_constant__ JbuFastArgs a)
 {
     constexpr int T = 2 * R + 1;
-    constexpr int P = S < 4 ? S : 4;  // pixels per thread along x
+    static_assert(S % P == 0, "a thread's P pixels must share one footprint");
     // NR rows per thread: rows 2t, 2t+1 of a tile are in one footprint row pair (S even)
     constexpr int NT = JB_X * JB_Y / NR;
     __shared__ uint2 sT[JB_LW * JB_LH];
@@ -440,32 +440,32 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? 5 : 3) k_jbu_vec(c
 }
 
 // ---------------------------------------------------------------- launch
-template <int S, int NR>
+template <int S, int NR, int P>
 static void launch_vec(int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo, const uint8_t *guide,
                        float *disp_hi, float *xyz, unsigned long long *n_valid, const JbuFastArgs &a)
 {
     const dim3 block(JB_X, JB_Y / NR);
     switch (radius) {
-    case 1: k_jbu_vec<1, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 2: k_jbu_vec<2, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 3: k_jbu_vec<3, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 4: k_jbu_vec<4, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 5: k_jbu_vec<5, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 6: k_jbu_vec<6, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 7: k_jbu_vec<7, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    default: k_jbu_vec<8, S, NR><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 1: k_jbu_vec<1, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 2: k_jbu_vec<2, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 3: k_jbu_vec<3, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 4: k_jbu_vec<4, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 5: k_jbu_vec<5, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 6: k_jbu_vec<6, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    case 7: k_jbu_vec<7, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    default: k_jbu_vec<8, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     }
 }
 
-template <int S>
+template <int S, int P>
 static void launch_vec_rows(int rows, int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo,
                             const uint8_t *guide, float *disp_hi, float *xyz, unsigned long long *n_valid,
                             const JbuFastArgs &a)
 {
     if (rows == 1)
-        launch_vec<S, 1>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        launch_vec<S, 1, P>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
     else
-        launch_vec<S, 2>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        launch_vec<S, 2, P>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
 }
 
 cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
@@ -497,7 +497,12 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     dim3 block(JB_X, JB_Y);
     // the vector kernel needs P-aligned guide words and 4P-byte aligned outputs
     const auto al = [](const void *p, uintptr_t m) { return ((uintptr_t)p & (m - 1)) == 0; };
-    const int P = s >= 4 ? 4 : 2;
+    // pixels per thread (tuning knob VSBP_JBU_P = 2 or 4 when s % 4 == 0; identical results)
+    static const int p_env = [] {
+        const char *e = getenv("VSBP_JBU_P");
+        return (e && e[0] == '2') ? 2 : 4;
+    }();
+    const int P = s >= 4 ? p_env : 2;
     const bool vec = (s == 2 || s == 4 || s == 8) && al(guide, P == 4 ? 4 : 2) && al(disp_hi, 4 * P) && al(xyz, 4 * P);
     if (vec) {
         // rows per thread of the vector kernel (tuning knob; both give identical results)
@@ -507,11 +512,15 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
         }();
         dim3 grid((W * s + JB_X * P - 1) / (JB_X * P), (H * s + JB_Y - 1) / JB_Y, B);
         if (s == 2)
-            launch_vec_rows<2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec_rows<2, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        else if (s == 4 && P == 4)
+            launch_vec_rows<4, 4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else if (s == 4)
-            launch_vec_rows<4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec_rows<4, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+        else if (P == 4)
+            launch_vec_rows<8, 4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else
-            launch_vec_rows<8>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec_rows<8, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
     } else {
         dim3 grid((W * s + JB_X - 1) / JB_X, (H * s + JB_Y - 1) / JB_Y, B);
         switch (radius) {
