@@ -440,32 +440,25 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? 5 : 8) :
 }
 
 // ---------------------------------------------------------------- launch
-template <int S, int NR, int P>
+// The vector kernel is instantiated for R <= JB_RVEC only (the paper's radii 2..5;
+// larger windows take the scalar kernel), two rows per thread and P = min(S, 4)
+// pixels per thread: the measured best of P in {2,4} x rows in {1,2}.
+// Each extra instantiation costs minutes of ptxas time at full unroll.
+constexpr int JB_RVEC = 5;
+
+template <int S, int P>
 static void launch_vec(int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo, const uint8_t *guide,
                        float *disp_hi, float *xyz, unsigned long long *n_valid, const JbuFastArgs &a)
 {
+    constexpr int NR = 2;
     const dim3 block(JB_X, JB_Y / NR);
     switch (radius) {
     case 1: k_jbu_vec<1, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     case 2: k_jbu_vec<2, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     case 3: k_jbu_vec<3, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     case 4: k_jbu_vec<4, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 5: k_jbu_vec<5, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 6: k_jbu_vec<6, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    case 7: k_jbu_vec<7, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
-    default: k_jbu_vec<8, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
+    default: k_jbu_vec<5, S, NR, P><<<grid, block, 0, st>>>(disp_lo, guide, disp_hi, xyz, n_valid, a); break;
     }
-}
-
-template <int S, int P>
-static void launch_vec_rows(int rows, int radius, dim3 grid, cudaStream_t st, const int32_t *disp_lo,
-                            const uint8_t *guide, float *disp_hi, float *xyz, unsigned long long *n_valid,
-                            const JbuFastArgs &a)
-{
-    if (rows == 1)
-        launch_vec<S, 1, P>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
-    else
-        launch_vec<S, 2, P>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
 }
 
 cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
@@ -497,30 +490,17 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     dim3 block(JB_X, JB_Y);
     // the vector kernel needs P-aligned guide words and 4P-byte aligned outputs
     const auto al = [](const void *p, uintptr_t m) { return ((uintptr_t)p & (m - 1)) == 0; };
-    // pixels per thread (tuning knob VSBP_JBU_P = 2 or 4 when s % 4 == 0; identical results)
-    static const int p_env = [] {
-        const char *e = getenv("VSBP_JBU_P");
-        return (e && e[0] == '2') ? 2 : 4;
-    }();
-    const int P = s >= 4 ? p_env : 2;
-    const bool vec = (s == 2 || s == 4 || s == 8) && al(guide, P == 4 ? 4 : 2) && al(disp_hi, 4 * P) && al(xyz, 4 * P);
+    const int P = s >= 4 ? 4 : 2;
+    const bool vec = (s == 2 || s == 4 || s == 8) && radius <= JB_RVEC && al(guide, P == 4 ? 4 : 2) &&
+                     al(disp_hi, 4 * P) && al(xyz, 4 * P);
     if (vec) {
-        // rows per thread of the vector kernel (tuning knob; both give identical results)
-        static const int rows = [] {
-            const char *e = getenv("VSBP_JBU_ROWS");
-            return (e && e[0] == '1') ? 1 : 2;
-        }();
         dim3 grid((W * s + JB_X * P - 1) / (JB_X * P), (H * s + JB_Y - 1) / JB_Y, B);
         if (s == 2)
-            launch_vec_rows<2, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
-        else if (s == 4 && P == 4)
-            launch_vec_rows<4, 4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec<2, 2>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else if (s == 4)
-            launch_vec_rows<4, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
-        else if (P == 4)
-            launch_vec_rows<8, 4>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec<4, 4>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else
-            launch_vec_rows<8, 2>(rows, radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
+            launch_vec<8, 4>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
     } else {
         dim3 grid((W * s + JB_X - 1) / JB_X, (H * s + JB_Y - 1) / JB_Y, B);
         switch (radius) {
