@@ -25,7 +25,8 @@ import numpy as np
 import torch
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "libvsbp.so")
+# VSBP_LIB: load another build of the same library (A/B timing experiments in tools/)
+LIB_PATH = os.environ.get("VSBP_LIB") or os.path.join(_HERE, "libvsbp.so")
 
 VSBP_OPT_MSG_BYTES = 1
 VSBP_OPT_KERNEL = 2

@@ -120,11 +120,12 @@ __global__ void k_icp_compact(const float *__restrict__ xyz, int n, const int *_
 struct IcpGrid {
     unsigned long long *keys;  // [HT]
     unsigned *count;           // [HT]
-    unsigned *start;           // [HT] (exclusive scan of count)
+    unsigned *start;           // [HT] first entry of the cell in pts (atomic allocation)
     unsigned *cursor;          // [HT]
-    int *pts;                  // [nt] target indices grouped by cell
+    unsigned *total;           // [1] allocation counter
+    double4 *pts;              // [nt] {x, y, z, index bits} grouped by cell (contiguous per cell)
     unsigned mask;
-    double inv_cell;
+    double inv_cell, cell;
 };
 
 // cell coordinates, clamped to the 21-bit key range (clamped points share border
@@ -155,6 +156,17 @@ __global__ void k_icp_insert(const double *__restrict__ Q, const int *__restrict
     }
 }
 
+// cell storage: each occupied cell gets a contiguous range of pts.  The ranges are
+// allocated with one atomic per cell, so their order in memory is arbitrary; the
+// pairing is order-independent (nearest by (d2, index)), so results are not.
+__global__ void k_icp_alloc(IcpGrid g)
+{
+    for (unsigned s = blockIdx.x * blockDim.x + threadIdx.x; s <= g.mask; s += gridDim.x * blockDim.x) {
+        const unsigned c = g.count[s];
+        if (c) g.start[s] = atomicAdd(g.total, c);
+    }
+}
+
 __global__ void k_icp_scatter(const double *__restrict__ Q, const int *__restrict__ nt_p, IcpGrid g)
 {
     const int nt = *nt_p;
@@ -164,7 +176,8 @@ __global__ void k_icp_scatter(const double *__restrict__ Q, const int *__restric
         const unsigned long long k = cell_key(c[0], c[1], c[2]);
         unsigned s = hash_slot(k, g.mask);
         while (g.keys[s] != k) s = (s + 1) & g.mask;
-        g.pts[g.start[s] + atomicAdd(g.cursor + s, 1u)] = i;
+        g.pts[g.start[s] + atomicAdd(g.cursor + s, 1u)] =
+            make_double4(Q[3 * i], Q[3 * i + 1], Q[3 * i + 2], __longlong_as_double((long long)i));
     }
 }
 
@@ -176,9 +189,15 @@ struct IcpState {
     int iters, done, converged, npairs;
 };
 
-__global__ void k_icp_pair(const double *__restrict__ S, const int *__restrict__ ns_p, const double *__restrict__ Q,
-                           IcpGrid g, const IcpState *__restrict__ st, double max_d2, int *__restrict__ match,
-                           double *__restrict__ dist2)
+// Nearest target of each transformed source point.  The 27 cells around p are
+// visited own cell first; a cell is skipped when its box is farther from p than the
+// best distance so far (or than max_dist): every point stored in it is at least
+// that far, so the nearest by (d2, index) is unchanged.  The box bound is reduced
+// by a margin of 1e-7 cells (far above the rounding of floor(x / cell)) and the
+// comparison is strict, so ties are never pruned.
+__global__ void __launch_bounds__(IC_T) k_icp_pair(const double *__restrict__ S, const int *__restrict__ ns_p,
+                                                    IcpGrid g, const IcpState *__restrict__ st, double max_d2,
+                                                    int *__restrict__ match, double *__restrict__ dist2)
 {
     if (st->done) return;
     const int ns = *ns_p;
@@ -192,26 +211,47 @@ __global__ void k_icp_pair(const double *__restrict__ S, const int *__restrict__
                     T[4 * a + 3]);
     long long c[3];
     cell_of(p, g.inv_cell, c);
+    // distance from p to the lower / upper face of its cell along each axis (>= 0)
+    double lo[3], hi[3];
+    bool prune = true;
+#pragma unroll
+    for (int a = 0; a < 3; ++a) {
+        const double f = floor(p[a] * g.inv_cell);
+        prune = prune && fabs(f) < 1048000.0;  // clamped cells: no geometry, visit all 27
+        const double m = 1e-7 * g.cell;
+        lo[a] = fmax(p[a] - (double)c[a] * g.cell - m, 0.0);
+        hi[a] = fmax((double)(c[a] + 1) * g.cell - p[a] - m, 0.0);
+    }
     double best = INFINITY;
     int bj = -1;
-    for (int dz = -1; dz <= 1; ++dz)
-        for (int dy = -1; dy <= 1; ++dy)
-            for (int dx = -1; dx <= 1; ++dx) {
-                const unsigned long long k = cell_key(c[0] + dx, c[1] + dy, c[2] + dz);
-                unsigned s = hash_slot(k, g.mask);
-                while (g.keys[s] != IC_EMPTY && g.keys[s] != k) s = (s + 1) & g.mask;
-                if (g.keys[s] != k) continue;
-                const unsigned b0 = g.start[s], b1 = b0 + g.count[s];
-                for (unsigned e = b0; e < b1; ++e) {
-                    const int j = g.pts[e];
-                    const double ex = dsub(p[0], Q[3 * j]), ey = dsub(p[1], Q[3 * j + 1]), ez = dsub(p[2], Q[3 * j + 2]);
-                    const double d2 = dadd(dadd(dmul(ex, ex), dmul(ey, ey)), dmul(ez, ez));
-                    if (d2 < best || (d2 == best && j < bj)) {
-                        best = d2;
-                        bj = j;
-                    }
-                }
+    for (int n = 0; n < 27; ++n) {
+        // n = 0 is the own cell, then the 26 neighbours
+        const int e = n == 0 ? 13 : (n <= 13 ? n - 1 : n);
+        const int dx = e % 3 - 1, dy = (e / 3) % 3 - 1, dz = e / 9 - 1;
+        if (prune) {
+            const double bx = dx < 0 ? lo[0] : (dx > 0 ? hi[0] : 0.0);
+            const double by = dy < 0 ? lo[1] : (dy > 0 ? hi[1] : 0.0);
+            const double bz = dz < 0 ? lo[2] : (dz > 0 ? hi[2] : 0.0);
+            const double bd2 = bx * bx + by * by + bz * bz;
+            if (bd2 > fmin(best, max_d2) * (1.0 + 1e-12)) continue;
+        }
+        const unsigned long long k = cell_key(c[0] + dx, c[1] + dy, c[2] + dz);
+        unsigned s = hash_slot(k, g.mask);
+        unsigned long long ks;
+        while ((ks = g.keys[s]) != IC_EMPTY && ks != k) s = (s + 1) & g.mask;
+        if (ks != k) continue;
+        const unsigned b0 = g.start[s], b1 = b0 + g.count[s];
+        for (unsigned e2 = b0; e2 < b1; ++e2) {
+            const double4 q = g.pts[e2];
+            const int j = (int)__double_as_longlong(q.w);
+            const double ex = dsub(p[0], q.x), ey = dsub(p[1], q.y), ez = dsub(p[2], q.z);
+            const double d2 = dadd(dadd(dmul(ex, ex), dmul(ey, ey)), dmul(ez, ez));
+            if (d2 < best || (d2 == best && j < bj)) {
+                best = d2;
+                bj = j;
             }
+        }
+    }
     const bool keep = bj >= 0 && best <= max_d2;
     match[i] = keep ? bj : -1;
     dist2[i] = keep ? best : 0.0;
@@ -333,27 +373,39 @@ __device__ void horn_rotation(const double H[9], double R[9])
                       {Szx - Sxz, Sxy + Syx, -Sxx + Syy - Szz, Syz + Szy},
                       {Sxy - Syx, Szx + Sxz, Syz + Szy, -Sxx - Syy + Szz}};
     double V[4][4] = {{1, 0, 0, 0}, {0, 1, 0, 0}, {0, 0, 1, 0}, {0, 0, 0, 1}};
+    // fully unrolled so N and V stay in registers (a local-memory version took
+    // ~150 us per solve); stop when the off-diagonal mass is negligible
+    double diag = 0.0;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) diag += N[i][i] * N[i][i];
     for (int sweep = 0; sweep < 50; ++sweep) {
         double off = 0.0;
+#pragma unroll
         for (int i = 0; i < 4; ++i)
+#pragma unroll
             for (int j = i + 1; j < 4; ++j) off += N[i][j] * N[i][j];
-        if (off == 0.0) break;
+        if (off <= 1e-40 * diag) break;
+#pragma unroll
         for (int p = 0; p < 4; ++p)
+#pragma unroll
             for (int q = p + 1; q < 4; ++q) {
                 if (N[p][q] == 0.0) continue;
                 const double theta = (N[q][q] - N[p][p]) / (2.0 * N[p][q]);
                 const double t = (theta >= 0 ? 1.0 : -1.0) / (fabs(theta) + sqrt(theta * theta + 1.0));
                 const double c = 1.0 / sqrt(t * t + 1.0), s = t * c;
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {  // columns p, q of N
                     const double a = N[k][p], b = N[k][q];
                     N[k][p] = c * a - s * b;
                     N[k][q] = s * a + c * b;
                 }
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {  // rows p, q
                     const double a = N[p][k], b = N[q][k];
                     N[p][k] = c * a - s * b;
                     N[q][k] = s * a + c * b;
                 }
+#pragma unroll
                 for (int k = 0; k < 4; ++k) {
                     const double a = V[k][p], b = V[k][q];
                     V[k][p] = c * a - s * b;
@@ -361,10 +413,14 @@ __device__ void horn_rotation(const double H[9], double R[9])
                 }
             }
     }
-    int m = 0;
+    // eigenvector of the largest eigenvalue (register selects, no dynamic indexing)
+    double w = V[0][0], x = V[1][0], y = V[2][0], z = V[3][0], lm = N[0][0];
+#pragma unroll
     for (int i = 1; i < 4; ++i)
-        if (N[i][i] > N[m][m]) m = i;
-    double w = V[0][m], x = V[1][m], y = V[2][m], z = V[3][m];
+        if (N[i][i] > lm) {
+            lm = N[i][i];
+            w = V[0][i], x = V[1][i], y = V[2][i], z = V[3][i];
+        }
     const double nrm = sqrt(w * w + x * x + y * y + z * z);
     w /= nrm, x /= nrm, y /= nrm, z /= nrm;
     R[0] = w * w + x * x - y * y - z * z;
@@ -435,8 +491,8 @@ size_t icp_workspace_bytes(int ns, int nt)
     add(sizeof(double) * 3 * (size_t)(nt > 0 ? nt : 1));  // Q
     add(sizeof(int) * (size_t)(nbs + nbt + 4));           // block counts + totals
     add(sizeof(unsigned long long) * ht);
-    add(sizeof(unsigned) * ht * 3);
-    add(sizeof(int) * (size_t)(nt > 0 ? nt : 1));
+    add(sizeof(unsigned) * (ht * 3 + 1));
+    add(sizeof(double4) * (size_t)(nt > 0 ? nt : 1));
     add(sizeof(int) * (size_t)(ns > 0 ? ns : 1));         // match
     add(sizeof(double) * (size_t)(ns > 0 ? ns : 1));      // dist2
     add(sizeof(double) * 9 * 1024);                       // partials
@@ -462,12 +518,14 @@ cudaError_t launch_icp(const float *src, int ns, const float *tgt, int nt, const
     int *blks = cnt, *blkt = cnt + nbs, *ns_d = cnt + nbs + nbt, *nt_d = ns_d + 1;
     IcpGrid g;
     g.keys = (unsigned long long *)take(sizeof(unsigned long long) * ht);
-    g.count = (unsigned *)take(sizeof(unsigned) * ht * 3);
+    g.count = (unsigned *)take(sizeof(unsigned) * (ht * 3 + 1));
     g.start = g.count + ht;
     g.cursor = g.start + ht;
-    g.pts = (int *)take(sizeof(int) * (size_t)(nt > 0 ? nt : 1));
+    g.total = g.cursor + ht;
+    g.pts = (double4 *)take(sizeof(double4) * (size_t)(nt > 0 ? nt : 1));
     g.mask = ht - 1;
     g.inv_cell = 1.0 / max_dist;
+    g.cell = max_dist;
     int *match = (int *)take(sizeof(int) * (size_t)(ns > 0 ? ns : 1));
     double *dist2 = (double *)take(sizeof(double) * (size_t)(ns > 0 ? ns : 1));
     double *part = (double *)take(sizeof(double) * 9 * 1024);
@@ -492,16 +550,15 @@ cudaError_t launch_icp(const float *src, int ns, const float *tgt, int nt, const
     k_icp_fix_ns<<<1, 1, 0, st>>>(ns_d, stride);
     // grid
     if ((e = cudaMemsetAsync(g.keys, 0xff, sizeof(unsigned long long) * ht, st)) != cudaSuccess) return e;
-    if ((e = cudaMemsetAsync(g.count, 0, sizeof(unsigned) * ht * 3, st)) != cudaSuccess) return e;
+    if ((e = cudaMemsetAsync(g.count, 0, sizeof(unsigned) * (ht * 3 + 1), st)) != cudaSuccess) return e;
     k_icp_insert<<<148 * 4, IC_T, 0, st>>>(Q, nt_d, g);
-    cudaMemcpyAsync(g.start, g.count, sizeof(unsigned) * ht, cudaMemcpyDeviceToDevice, st);
-    k_icp_scan<<<1, 1024, 0, st>>>((int *)g.start, (int)ht, nt_d + 1);
+    k_icp_alloc<<<148 * 4, IC_T, 0, st>>>(g);
     k_icp_scatter<<<148 * 4, IC_T, 0, st>>>(Q, nt_d, g);
-    note_launch(12);
+    note_launch(10);
     const int nb = 148 * 4 < 1024 ? 148 * 4 : 1024;
     const double max_d2 = max_dist * max_dist;
     for (int it = 1; it <= max_iter; ++it) {
-        k_icp_pair<<<(ns + IC_T - 1) / IC_T, IC_T, 0, st>>>(S, ns_d, Q, g, state, max_d2, match, dist2);
+        k_icp_pair<<<(ns + IC_T - 1) / IC_T, IC_T, 0, st>>>(S, ns_d, g, state, max_d2, match, dist2);
         k_icp_sum1<<<nb, IC_T, 0, st>>>(S, ns_d, Q, state, match, dist2, part);
         k_icp_centroid<<<1, IC_T, 0, st>>>(part, nb, state);
         k_icp_sum2<<<nb, IC_T, 0, st>>>(S, ns_d, Q, state, match, part);

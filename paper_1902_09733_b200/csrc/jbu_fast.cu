@@ -59,19 +59,22 @@ __device__ __forceinline__ float ex2(float x)
     return y;
 }
 
-// stage the block's low-res taps: {guide RGB at the footprint's centre sample, label as f32}
+// stage the block's low-res taps: {guide RGB at the footprint's centre sample, label as f32}.
+// Taps outside the low-res image get weight 0 (row factor 0 or column exponent -inf),
+// but their record must keep the weighted sums finite: it is a copy of the nearest
+// in-image tap (clamped coordinates), which lies in every window that contains the
+// phantom, so its colour distance is >= the window minimum and its exponent never
+// overflows (0 * inf would be NaN).
 __device__ __forceinline__ void stage_taps(uint2 *sT, const uint8_t *G, const int32_t *Dl, int lx0, int ly0, int lw,
                                            int lh, int s, int Wh, const JbuFastArgs &a, int nthreads)
 {
     const int tid = threadIdx.y * JB_X + threadIdx.x;
     for (int e = tid; e < lw * lh; e += nthreads) {
-        const int qy = ly0 + e / lw, qx = lx0 + e % lw;
-        uint2 rec = make_uint2(0u, 0u);
-        if (qx >= 0 && qy >= 0 && qx < a.W && qy < a.H) {
-            const uint8_t *g = G + ((size_t)(s * qy + s / 2) * Wh + (size_t)(s * qx + s / 2)) * 3;
-            rec.x = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
-            rec.y = __float_as_uint((float)Dl[(size_t)qy * a.W + qx]);
-        }
+        const int qy = min(max(ly0 + e / lw, 0), a.H - 1), qx = min(max(lx0 + e % lw, 0), a.W - 1);
+        const uint8_t *g = G + ((size_t)(s * qy + s / 2) * Wh + (size_t)(s * qx + s / 2)) * 3;
+        uint2 rec;
+        rec.x = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
+        rec.y = __float_as_uint((float)Dl[(size_t)qy * a.W + qx]);
         sT[e] = rec;
     }
 }

@@ -234,6 +234,30 @@ def test_jbu_vector_path_equals_scalar_path(s, r):
     assert torch.equal(vec, sca)
 
 
+@pytest.mark.parametrize("s,r", [(4, 2), (2, 3), (8, 1), (4, 5)])
+def test_jbu_far_pixels_vector_equals_scalar_and_oracle(s, r):
+    """A guide of saturated random colours makes most pixels "far" (centre tap far in
+    colour, handled warp-cooperatively by far_pixel) next to near ones in the same
+    warp: both kernels bit-identical, and within 1e-4 px of the oracle."""
+    rng = np.random.default_rng(11 * s + r)
+    H, W = 19, 29
+    # output disparities below 256 px like every BASELINE config (s*L <= 256): the
+    # f32 kernel's error is relative (~2e-7), so 1e-4 px holds up to 256 (DESIGN §5)
+    lo_np = rng.integers(0, 256 // s, size=(H, W)).astype(np.int32)
+    g = np.where(rng.random((H * s, W * s, 3)) < 0.5, 0, 255).astype(np.uint8)
+    g[: H * s // 2] = synthgen.value_noise_rgb(3, W * s, H * s)[: H * s // 2]  # near half
+    guide = np.ascontiguousarray(g)
+    lo, gd = to_dev(lo_np), to_dev(guide)
+    vec = P.jbu_upsample(lo, gd, s, 3.75, 15.0, r)
+    buf = torch.empty(H * s * W * s + 1, dtype=torch.float32, device=dev())
+    sca = P.jbu_upsample(lo, gd, s, 3.75, 15.0, r, out=buf[1:].view(1, H * s, W * s))
+    assert not torch.isnan(vec).any() and not torch.isnan(sca).any()
+    bad = torch.nonzero(vec.reshape(sca.shape) != sca)
+    assert bad.numel() == 0, f"vector != scalar at {bad[:8].tolist()}"
+    ref = oracle.jbu(lo_np, guide, s, 3.75, 15.0, r)
+    assert np.max(np.abs(vec.reshape(ref.shape).cpu().numpy().astype(np.float64) - ref)) <= 1e-4
+
+
 def test_jbu_full_frame_config3():
     left, _, d_lo = synthgen.stereo_pair_rgb(2)
     got = P.jbu_upsample(to_dev(d_lo), to_dev(left), 4, 3.75, 15.0, 2).cpu().numpy().astype(np.float64)

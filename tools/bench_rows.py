@@ -79,16 +79,15 @@ def main():
     res["f3_harris_only"] = {"ms_per_pair": timed(lambda: P.harris_corners(gl, 30, 30, 4, 10 ** 9)) / B}
 
     # f4: ICP of a low-res Eq.3 cloud against itself moved by a small rigid motion
-    import oracle  # test infrastructure: only to build the input cloud (Eq.3 in double)
     I = synthgen.INTRINSICS
-    Q = oracle.q_matrix(I["f_du"] / 4, I["f_dv"] / 4, (I["u0"] + 0.5) / 4 - 0.5, (I["v0"] + 0.5) / 4 - 0.5, I["B"])
-    d = out[0].cpu().numpy().astype(np.float64)
-    xyz, _ = oracle.reproject(d, Q, 1.0)
-    src = xyz.reshape(-1, 3).astype(np.float32)
+    Q = P.q_matrix(I["f_du"] / 4, I["f_dv"] / 4, (I["u0"] + 0.5) / 4 - 0.5, (I["v0"] + 0.5) / 4 - 0.5, I["B"])
+    xyz, _ = P.reproject(out[0].float().contiguous(), Q, 1.0)  # Eq.3 on the GPU (a7)
+    S = xyz.reshape(-1, 3).contiguous()
+    src = S.cpu().numpy()
     th = np.deg2rad(0.3)
-    Rm = np.array([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]])
-    tgt = (src.astype(np.float64) @ Rm.T + [0.05, 0.02, -0.03]).astype(np.float32)
-    S, T = torch.from_numpy(src).to(dev), torch.from_numpy(tgt).to(dev)
+    Rm = torch.tensor([[np.cos(th), -np.sin(th), 0], [np.sin(th), np.cos(th), 0], [0, 0, 1]], dtype=torch.float64,
+                      device=dev)
+    T = (S.double() @ Rm.T + torch.tensor([0.05, 0.02, -0.03], dtype=torch.float64, device=dev)).float().contiguous()
     ms = timed(lambda: P.icp_register(S, T, max_iter=20, max_dist=0.25, eps=1e-7, stride=4), reps=5)
     o = P.icp_register(S, T, max_iter=20, max_dist=0.25, eps=1e-7, stride=4).cpu().numpy()
     res["f4_icp_lowres_cloud"] = {"ms_per_registration": ms, "points": int(np.sum(~np.isnan(src[:, 0]))),
