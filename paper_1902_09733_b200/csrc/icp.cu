@@ -189,20 +189,34 @@ struct IcpState {
     int iters, done, converged, npairs;
 };
 
-// Nearest target of each transformed source point.  The 27 cells around p are
-// visited own cell first; a cell is skipped when its box is farther from p than the
-// best distance so far (or than max_dist): every point stored in it is at least
-// that far, so the nearest by (d2, index) is unchanged.  The box bound is reduced
-// by a margin of 1e-7 cells (far above the rounding of floor(x / cell)) and the
-// comparison is strict, so ties are never pruned.
+// Nearest target of each transformed source point, IC_G lanes per point (the lanes
+// split each cell's points; (d2, index) is reduced over the group after every cell,
+// so every lane prunes with the group's best).  The 27 cells around p are visited
+// own cell first; a cell is skipped when its box is farther from p than the best
+// distance so far (or than max_dist): every point stored in it is at least that far,
+// so the nearest by (d2, index) is unchanged.  The box bound is reduced by a margin
+// of 1e-7 cells (far above the rounding of floor(x / cell)) and the comparison is
+// strict, so ties are never pruned.
+constexpr int IC_G = 8;
+
+__device__ __forceinline__ void better(double &best, int &bj, double d2, int j)
+{
+    if (d2 < best || (d2 == best && (unsigned)j < (unsigned)bj)) {
+        best = d2;
+        bj = j;
+    }
+}
+
 __global__ void __launch_bounds__(IC_T) k_icp_pair(const double *__restrict__ S, const int *__restrict__ ns_p,
                                                     IcpGrid g, const IcpState *__restrict__ st, double max_d2,
                                                     int *__restrict__ match, double *__restrict__ dist2)
 {
     if (st->done) return;
     const int ns = *ns_p;
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= ns) return;
+    const int i = (blockIdx.x * blockDim.x + threadIdx.x) / IC_G;
+    const int lg = threadIdx.x & (IC_G - 1);
+    if (i >= ns) return;  // whole groups exit together (IC_G divides the block)
+    const unsigned gmask = (0xFFFFFFFFu >> (32 - IC_G)) << ((threadIdx.x & 31) & ~(IC_G - 1));
     const double *T = st->T;
     double p[3];
 #pragma unroll
@@ -223,7 +237,7 @@ __global__ void __launch_bounds__(IC_T) k_icp_pair(const double *__restrict__ S,
         hi[a] = fmax((double)(c[a] + 1) * g.cell - p[a] - m, 0.0);
     }
     double best = INFINITY;
-    int bj = -1;
+    int bj = -1;  // as unsigned: larger than every index
     for (int n = 0; n < 27; ++n) {
         // n = 0 is the own cell, then the 26 neighbours
         const int e = n == 0 ? 13 : (n <= 13 ? n - 1 : n);
@@ -241,20 +255,20 @@ __global__ void __launch_bounds__(IC_T) k_icp_pair(const double *__restrict__ S,
         while ((ks = g.keys[s]) != IC_EMPTY && ks != k) s = (s + 1) & g.mask;
         if (ks != k) continue;
         const unsigned b0 = g.start[s], b1 = b0 + g.count[s];
-        for (unsigned e2 = b0; e2 < b1; ++e2) {
+        for (unsigned e2 = b0 + lg; e2 < b1; e2 += IC_G) {
             const double4 q = g.pts[e2];
-            const int j = (int)__double_as_longlong(q.w);
             const double ex = dsub(p[0], q.x), ey = dsub(p[1], q.y), ez = dsub(p[2], q.z);
-            const double d2 = dadd(dadd(dmul(ex, ex), dmul(ey, ey)), dmul(ez, ez));
-            if (d2 < best || (d2 == best && j < bj)) {
-                best = d2;
-                bj = j;
-            }
+            better(best, bj, dadd(dadd(dmul(ex, ex), dmul(ey, ey)), dmul(ez, ez)), (int)__double_as_longlong(q.w));
         }
+#pragma unroll
+        for (int o = IC_G / 2; o > 0; o >>= 1)
+            better(best, bj, __shfl_xor_sync(gmask, best, o, IC_G), __shfl_xor_sync(gmask, bj, o, IC_G));
     }
-    const bool keep = bj >= 0 && best <= max_d2;
-    match[i] = keep ? bj : -1;
-    dist2[i] = keep ? best : 0.0;
+    if (lg == 0) {
+        const bool keep = bj >= 0 && best <= max_d2;
+        match[i] = keep ? bj : -1;
+        dist2[i] = keep ? best : 0.0;
+    }
 }
 
 // block sums of K doubles in a fixed tree order (deterministic)
@@ -558,7 +572,7 @@ cudaError_t launch_icp(const float *src, int ns, const float *tgt, int nt, const
     const int nb = 148 * 4 < 1024 ? 148 * 4 : 1024;
     const double max_d2 = max_dist * max_dist;
     for (int it = 1; it <= max_iter; ++it) {
-        k_icp_pair<<<(ns + IC_T - 1) / IC_T, IC_T, 0, st>>>(S, ns_d, g, state, max_d2, match, dist2);
+        k_icp_pair<<<(unsigned)(((long)ns * IC_G + IC_T - 1) / IC_T), IC_T, 0, st>>>(S, ns_d, g, state, max_d2, match, dist2);
         k_icp_sum1<<<nb, IC_T, 0, st>>>(S, ns_d, Q, state, match, dist2, part);
         k_icp_centroid<<<1, IC_T, 0, st>>>(part, nb, state);
         k_icp_sum2<<<nb, IC_T, 0, st>>>(S, ns_d, Q, state, match, part);
