@@ -189,14 +189,22 @@ __device__ __forceinline__ void store_pairs(void *base, int bytes, size_t off, c
     }
 }
 
-template <bool PAD>
+// 32-bit element offset of (colour c, row y, colour-column i) within one pair (the
+// per-pair arrays are < 2^32 elements; the pair base is added once in 64 bits)
+__device__ __forceinline__ uint32_t d_off32(int c, int y, int i, int H, int Wc, int Lp)
+{
+    return (((uint32_t)c * (uint32_t)H + (uint32_t)y) * (uint32_t)Wc + (uint32_t)i) * (uint32_t)Lp;
+}
+
+// NCH_T > 0: the chunk count is a compile-time power of two (shifts instead of divides)
+template <bool PAD, int NCH_T>
 __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict__ left,
                                                       const uint8_t *__restrict__ right, CostPyrArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int b = blockIdx.z;
     const int X0 = blockIdx.x * CP_T, Y0 = blockIdx.y * CP_T;
-    const int L = a.L, Lp = a.Lp, nch = a.nch;
+    const int L = a.L, Lp = a.Lp, nch = NCH_T > 0 ? NCH_T : a.nch;
     const int W = a.W[0], H = a.H[0];
     const int span = Lp + CP_T - 9;        // columns i = X0-Lp+9 .. X0+15
     const int i0 = X0 - Lp + 9;
@@ -209,23 +217,30 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
         const int x = X0 + (e & (CP_T - 1)), y = Y0 + e / CP_T;
         sl[e] = (x < W && y < H) ? __ldg(lb + (size_t)y * W + x) : 0;
     }
-    for (int e = threadIdx.x; e < CP_T * span; e += blockDim.x) {
-        const int r = e / span, j = e - r * span;
-        const int i = i0 + j, y = Y0 + r;
-        int v0 = 0, v1 = 0;
-        if (y < H) {
-            v0 = i < 0 ? CPF_SENT : (i < W ? (int)__ldg(rb + (size_t)y * W + i) : 0);
-            v1 = i - 8 < 0 ? CPF_SENT : (i - 8 < W ? (int)__ldg(rb + (size_t)y * W + i - 8) : 0);
+    // one warp per row (no division per entry; ~1/3 of the kernel's instructions
+    // went to a flat loop here)
+    for (int r = threadIdx.x >> 5; r < CP_T; r += blockDim.x >> 5) {
+        const int y = Y0 + r;
+        const uint8_t *rrow = rb + (size_t)min(y, H - 1) * W;
+        for (int j = threadIdx.x & 31; j < span; j += 32) {
+            const int i = i0 + j;
+            int v0 = 0, v1 = 0;
+            if (y < H) {
+                v0 = i < 0 ? CPF_SENT : (i < W ? (int)__ldg(rrow + i) : 0);
+                v1 = i - 8 < 0 ? CPF_SENT : (i - 8 < W ? (int)__ldg(rrow + i - 8) : 0);
+            }
+            sr[r * span + j] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
         }
-        sr[e] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
     }
     __syncthreads();
 
     const uint32_t T2 = (uint32_t)a.tau_d | ((uint32_t)a.tau_d << 16);
     const uint32_t lam = (uint32_t)a.lam_q;
     constexpr int TQ = CP_T / 2;
+    uint8_t *D0 = (uint8_t *)a.D[0] + (size_t)b * a.pairD[0] * a.dbytes[0];
+    uint8_t *D1 = a.F > 1 ? (uint8_t *)a.D[1] + (size_t)b * a.pairD[1] * a.dbytes[1] : nullptr;
     for (int it = threadIdx.x; it < TQ * TQ * nch; it += blockDim.x) {
-        const int q = it / nch, k = it - q * nch;
+        const int q = NCH_T > 0 ? it / NCH_T : it / nch, k = it - q * nch;
         const int qx = q % TQ, qy = q / TQ;
         uint32_t mask[8];
 #pragma unroll
@@ -263,16 +278,13 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
                     if (PAD) r[j] &= mask[j];
                     acc[j] += r[j];
                 }
-                if (a.write0) store_pairs(a.D[0], a.dbytes[0],
-                            (size_t)b * a.pairD[0] + d_off(0, (x + y) & 1, y, x >> 1, H, a.Wc[0], Lp) + k * CH, r);
+                if (a.write0) store_pairs(D0, a.dbytes[0], d_off32((x + y) & 1, y, x >> 1, H, a.Wc[0], Lp) + k * CH, r);
             }
         }
         if (a.F > 1) {
             const int X = (X0 >> 1) + qx, Y = (Y0 >> 1) + qy;
             if (X < a.W[1] && Y < a.H[1])
-                store_pairs(a.D[1], a.dbytes[1],
-                            (size_t)b * a.pairD[1] + d_off(0, (X + Y) & 1, Y, X >> 1, a.H[1], a.Wc[1], Lp) + k * CH,
-                            acc);
+                store_pairs(D1, a.dbytes[1], d_off32((X + Y) & 1, Y, X >> 1, a.H[1], a.Wc[1], Lp) + k * CH, acc);
             if (a.F > 2) {
                 int4 *dst = reinterpret_cast<int4 *>(sD + (size_t)q * Lp + k * CH);
                 dst[0] = make_int4(acc[0] & 0xFFFF, acc[1] & 0xFFFF, acc[2] & 0xFFFF, acc[3] & 0xFFFF);
@@ -315,17 +327,24 @@ cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArg
     const size_t smem = costpyr_smem(a.L, a.Lp, a.F);
     if (smem > 48 * 1024) {
         cudaError_t e = cudaFuncSetAttribute(k_costpyr, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_costpyr_fast<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-        if (e == cudaSuccess)
-            e = cudaFuncSetAttribute(k_costpyr_fast<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+        const void *fs[] = {(const void *)k_costpyr_fast<false, 0>, (const void *)k_costpyr_fast<false, 1>,
+                            (const void *)k_costpyr_fast<false, 2>, (const void *)k_costpyr_fast<false, 4>,
+                            (const void *)k_costpyr_fast<false, 8>, (const void *)k_costpyr_fast<true, 0>};
+        for (const void *f : fs)
+            if (e == cudaSuccess) e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
         if (e != cudaSuccess) return e;
     }
     dim3 grid((a.W[0] + CP_T - 1) / CP_T, (a.H[0] + CP_T - 1) / CP_T, B);
-    if (costpyr_fast_ok(a) && a.L % CH == 0)
-        k_costpyr_fast<false><<<grid, 256, smem, st>>>(left, right, a);
-    else if (costpyr_fast_ok(a))
-        k_costpyr_fast<true><<<grid, 256, smem, st>>>(left, right, a);
+    if (costpyr_fast_ok(a) && a.L % CH == 0) {
+        switch (a.nch) {
+        case 1: k_costpyr_fast<false, 1><<<grid, 256, smem, st>>>(left, right, a); break;
+        case 2: k_costpyr_fast<false, 2><<<grid, 256, smem, st>>>(left, right, a); break;
+        case 4: k_costpyr_fast<false, 4><<<grid, 256, smem, st>>>(left, right, a); break;
+        case 8: k_costpyr_fast<false, 8><<<grid, 256, smem, st>>>(left, right, a); break;
+        default: k_costpyr_fast<false, 0><<<grid, 256, smem, st>>>(left, right, a); break;
+        }
+    } else if (costpyr_fast_ok(a))
+        k_costpyr_fast<true, 0><<<grid, 256, smem, st>>>(left, right, a);
     else
         k_costpyr<<<grid, 256, smem, st>>>(left, right, a);
     note_launch();
