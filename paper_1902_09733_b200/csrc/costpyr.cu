@@ -160,13 +160,14 @@ __global__ void __launch_bounds__(256) k_costpyr(const uint8_t *__restrict__ lef
 // register as s16x2 on the DPX datapath, in the chunk order of vsbp_internal.cuh:
 // r_j = (label 16k+j | label 16k+j+8 << 16), which is the u16 storage word j and
 // one PRMT away from the u8 storage.  The staged right row holds, per column i,
-// the pair (R(i), R(i-8)) as s16x2, so for a pixel with grey l
-//   min(|l - r|, tau_d) = max(min((l+1) + ~r, tau_d), min(-l + r, tau_d))
-// (~r = -r-1 per half) is a LOP3, two VIADDMNMX and a VIMNMX per label pair, and
-// the data weight one IMAD of the packed pair.  The two pixels of a quad row share
-// 9 of their 16 column reads.  Columns left of the image hold r = -2048: both mins
-// give tau_d there, i.e. the border cost lambda_q * tau_d (R-8).
-constexpr int CPF_SENT = -2048;
+// the pair (lambda_q R(i), lambda_q R(i-8)) as s16x2, so for a pixel with grey l
+//   lambda_q min(|l - r|, tau_d) = max(min((lambda_q l + 1) + ~(lambda_q r), lambda_q tau_d),
+//                                      min(-lambda_q l + lambda_q r, lambda_q tau_d))
+// (~v = -v-1 per half; the data weight distributes over |.| and min) is two
+// VIADDMNMX and a VIMNMX per label pair plus the accumulation.  The two pixels of a
+// quad row share 9 of their 16 column reads.  Columns left of the image hold
+// -lambda_q tau_d: both mins give lambda_q tau_d there, the border cost (R-8).
+// Host check: lambda_q (255 + tau_d) < 2^15, so no half overflows.
 
 __device__ __forceinline__ uint32_t cp_prmt(uint32_t a, uint32_t b, uint32_t sel)
 {
@@ -207,9 +208,10 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
     const int L = a.L, Lp = a.Lp, nch = NCH_T > 0 ? NCH_T : a.nch;
     const int W = a.W[0], H = a.H[0];
     const int span = Lp + CP_T - 9;        // columns i = X0-Lp+9 .. X0+15
+    const int spanp = (span + 3) & ~3;     // row stride (16-byte rows)
     const int i0 = X0 - Lp + 9;
     uint8_t *sl = smem;                     // [16][16]
-    uint32_t *sr = reinterpret_cast<uint32_t *>(smem + CP_T * CP_T);  // [16][span]: (R(i), R(i-8)) as s16x2
+    uint32_t *sr = reinterpret_cast<uint32_t *>(smem + CP_T * CP_T);  // [16][spanp]: lambda_q (R(i), R(i-8)) as s16x2
     int *sD = reinterpret_cast<int *>(smem + a.img_smem);
     const uint8_t *lb = left + (size_t)b * H * W;
     const uint8_t *rb = right + (size_t)b * H * W;
@@ -217,25 +219,51 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
         const int x = X0 + (e & (CP_T - 1)), y = Y0 + e / CP_T;
         sl[e] = (x < W && y < H) ? __ldg(lb + (size_t)y * W + x) : 0;
     }
-    // one warp per row (no division per entry; ~1/3 of the kernel's instructions
-    // went to a flat loop here)
+    // right rows: one warp per row.  Fast path (W % 4 == 0, 4-byte aligned rows,
+    // span + 9 <= 256): every lane issues its (at most two) aligned 32-bit loads of
+    // the row window up front and the entries are assembled from them with
+    // shuffles, so the warp waits on one load latency instead of a chain of byte
+    // loads (the byte loop below was long-scoreboard bound).
+    const int lam_i = a.lam_q, sent = -a.lam_q * a.tau_d;
+    const int lane = threadIdx.x & 31;
+    const bool wpath = (W & 3) == 0 && span + 9 <= 256 && (((uintptr_t)rb) & 3) == 0;
     for (int r = threadIdx.x >> 5; r < CP_T; r += blockDim.x >> 5) {
         const int y = Y0 + r;
-        const uint8_t *rrow = rb + (size_t)min(y, H - 1) * W;
-        for (int j = threadIdx.x & 31; j < span; j += 32) {
-            const int i = i0 + j;
-            int v0 = 0, v1 = 0;
-            if (y < H) {
-                v0 = i < 0 ? CPF_SENT : (i < W ? (int)__ldg(rrow + i) : 0);
-                v1 = i - 8 < 0 ? CPF_SENT : (i - 8 < W ? (int)__ldg(rrow + i - 8) : 0);
+        if (y >= H) continue;  // rows below the image are never read
+        const uint8_t *rrow = rb + (size_t)y * W;
+        if (wpath) {
+            const int a0 = i0 - 9;  // multiple of 4: X0 % 16 == 0 and Lp % 16 == 0
+            uint32_t w[2];
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int c = a0 + 4 * (lane + 32 * h);  // words are wholly inside or outside [0, W)
+                w[h] = (c >= 0 && c < W && c < i0 + span) ? __ldg(reinterpret_cast<const uint32_t *>(rrow + c)) : 0u;
             }
-            sr[r * span + j] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
+            for (int jb = 0; jb < span; jb += 32) {  // warp-uniform trip count (shuffles)
+                const int j = jb + lane;
+                const int i = i0 + j;
+                const int b0 = j + 9, b1 = j + 1;  // byte positions of R(i), R(i-8) in the window
+                const uint32_t s0l = __shfl_sync(FULL, w[0], (b0 >> 2) & 31), s0h = __shfl_sync(FULL, w[1], (b0 >> 2) & 31);
+                const uint32_t s1l = __shfl_sync(FULL, w[0], (b1 >> 2) & 31), s1h = __shfl_sync(FULL, w[1], (b1 >> 2) & 31);
+                const uint32_t r0 = ((b0 >> 2) >= 32 ? s0h : s0l) >> (8 * (b0 & 3)) & 0xFFu;
+                const uint32_t r1 = ((b1 >> 2) >= 32 ? s1h : s1l) >> (8 * (b1 & 3)) & 0xFFu;
+                const int v0 = i < 0 ? sent : (i < W ? lam_i * (int)r0 : 0);
+                const int v1 = i - 8 < 0 ? sent : (i - 8 < W ? lam_i * (int)r1 : 0);
+                if (j < span) sr[r * spanp + j] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
+            }
+        } else {
+            for (int j = lane; j < span; j += 32) {
+                const int i = i0 + j;
+                const int v0 = i < 0 ? sent : (i < W ? lam_i * (int)__ldg(rrow + i) : 0);
+                const int v1 = i - 8 < 0 ? sent : (i - 8 < W ? lam_i * (int)__ldg(rrow + i - 8) : 0);
+                sr[r * spanp + j] = ((uint32_t)v0 & 0xFFFFu) | ((uint32_t)v1 << 16);
+            }
         }
     }
     __syncthreads();
 
-    const uint32_t T2 = (uint32_t)a.tau_d | ((uint32_t)a.tau_d << 16);
-    const uint32_t lam = (uint32_t)a.lam_q;
+    const uint32_t lt = (uint32_t)(a.lam_q * a.tau_d);
+    const uint32_t T2 = lt | (lt << 16);
     constexpr int TQ = CP_T / 2;
     uint8_t *D0 = (uint8_t *)a.D[0] + (size_t)b * a.pairD[0] * a.dbytes[0];
     uint8_t *D1 = a.F > 1 ? (uint8_t *)a.D[1] + (size_t)b * a.pairD[1] * a.dbytes[1] : nullptr;
@@ -254,7 +282,7 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
             const int py = 2 * qy + jy, y = Y0 + py;
             if (y >= H) continue;
             // columns x0q+1-16k-jj, jj = 0..8: pixel jx=1 uses jj = j, pixel jx=0 uses jj = j+1
-            const uint32_t *col = sr + py * span + (X0 + 2 * qx + 1 - k * CH - i0);
+            const uint32_t *col = sr + py * spanp + (X0 + 2 * qx + 1 - k * CH - i0);
             uint32_t e[9], ne[9];
 #pragma unroll
             for (int jj = 0; jj < 9; ++jj) {
@@ -265,7 +293,7 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
             for (int jx = 0; jx < 2; ++jx) {
                 const int px = 2 * qx + jx, x = X0 + px;
                 if (x >= W) continue;
-                const uint32_t lv = sl[py * CP_T + px];
+                const uint32_t lv = (uint32_t)lam_i * sl[py * CP_T + px];
                 const uint32_t lp1 = (lv + 1u) * 0x00010001u;
                 const uint32_t nl2 = ((0u - lv) & 0xFFFFu) * 0x00010001u;
                 uint32_t r[8];
@@ -274,7 +302,7 @@ __global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict_
                     const int jj = j + 1 - jx;
                     const uint32_t lo = __viaddmin_s16x2(lp1, ne[jj], T2);  // min(l - r, tau_d)
                     const uint32_t hi = __viaddmin_s16x2(nl2, e[jj], T2);   // min(r - l, tau_d)
-                    r[j] = __vmaxs2(lo, hi) * lam;
+                    r[j] = __vmaxs2(lo, hi);
                     if (PAD) r[j] &= mask[j];
                     acc[j] += r[j];
                 }
@@ -301,6 +329,7 @@ bool costpyr_fast_ok(const CostPyrArgs &a)
 {
     const long long lt = (long long)a.lam_q * a.tau_d;
     if (a.tau_d > 1000 || a.dbytes[0] > 2 || lt > 65535) return false;
+    if ((long long)a.lam_q * (255 + a.tau_d) + 1 >= 32768) return false;  // s16 halves of the staged row
     if (a.F > 1 && (a.dbytes[1] > 2 || 4 * lt > 65535)) return false;
     return true;
 }
@@ -308,7 +337,7 @@ bool costpyr_fast_ok(const CostPyrArgs &a)
 static size_t img_bytes(int L, int Lp)
 {
     const size_t generic = (size_t)CP_T * CP_T + (size_t)CP_T * (CP_T + L - 1);
-    const size_t fast = (size_t)CP_T * CP_T + (size_t)CP_T * (Lp + CP_T - 9) * 4;
+    const size_t fast = (size_t)CP_T * CP_T + (size_t)CP_T * ((Lp + CP_T - 9 + 3) & ~3) * 4;
     const size_t m = generic > fast ? generic : fast;
     return (m + 15) & ~(size_t)15;
 }
