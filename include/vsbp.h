@@ -82,6 +82,16 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        D_0.  Results are identical; 1 trades 11 % of the level-0
  *                        bytes for ~10 % more ALU work and measured slower. */
 #define VSBP_OPT_DIMG 3
+/*   VSBP_OPT_FINAL     : 1 = the last level-0 iteration is fused with the WTA of
+ *                        both colours (k_final_fast): its messages go straight into
+ *                        the receivers' beliefs and are never stored, so
+ *                        bp_get_messages(level 0) returns VSBP_EINVAL after such a
+ *                        call; 0 (default) = store them and label in separate passes.
+ *                        Disparities are identical; 1 moves 57 % fewer bytes but
+ *                        recomputes each colour-A pixel's belief for each of its four
+ *                        receivers and measured slower.  Applies when the packed
+ *                        kernels run with u8 level-0 costs, iters >= 2 and W >= 2. */
+#define VSBP_OPT_FINAL 4
 int bp_set_option(vsbp_bp *ctx, int option, int value);
 
 /* Quantised parameters: out[0..7] = {lambda_q, tau_d, tau_q, S, msg_bytes,
@@ -102,7 +112,8 @@ int bp_set_workspace(vsbp_bp *ctx, void *dptr, size_t bytes, int batch);
  *   disp        : int32 [B][H][W] labels, the WTA argmin of Eq.1's E_X(d)
  *                 (P:34), ties -> smallest d (R-13)
  * Requires a workspace bound for >= B pairs (else VSBP_EDIM).
- * The per-level message fields stay in the workspace for bp_get_messages.
+ * The per-level message fields stay in the workspace for bp_get_messages
+ * (level 0 only with VSBP_OPT_FINAL = 0).
  * bp_disparity is the B = 1 case.
  * ------------------------------------------------------------------------- */
 int bp_disparity_batch(vsbp_bp *ctx, int B, const uint8_t *left, const uint8_t *right, int32_t *disp,

@@ -284,6 +284,173 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
     }
 }
 
+// ---------------------------------------------------------------- fused final iteration (a4 + a5)
+// The last level-0 iteration updates colour A and is followed only by the WTA of
+// both colours, so its messages are consumed once, by the WTA of their receivers.
+// k_final_fast therefore never stores them: one G-lane group per colour-B pixel p
+// computes the four messages m_{q->p} of its colour-A neighbours q itself (the same
+// arithmetic as k_update_fast: h_q = D_q + the three incoming of q other than p's,
+// normalise, 3-tap envelope), adds them to D_p and takes p's WTA; the group also
+// labels its right neighbour q (belief h_q + m_{p->q}), and the pixel at x = 1 its
+// left neighbour (x = 0), so every colour-A pixel is labelled exactly once.
+// HBM per pixel pair: D_A, D_B and the four colour-B message planes (6L bytes at
+// u8) instead of 9L (last update) + 5L (WTA of the other colour); each colour-A
+// pixel's data is re-read by its four neighbours from L1/L2.  Requires W >= 2.
+template <bool PAD, bool SIGNED>
+__device__ __forceinline__ void one_message(const FastArgs &a, uint32_t h[8], const uint32_t padm[8], int lane_g,
+                                            uint32_t out[8])
+{
+    uint32_t m = chunk_min(h);
+    for (int s = a.G >> 1; s > 0; s >>= 1) m = __vminu2(m, __shfl_xor_sync(FULL, m, s, a.G));
+    if (SIGNED) {
+        const uint32_t neg = prmt(0u - m, 0u, 0x1010);
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = (uint32_t)__viaddmin_s16x2(h[j], neg, a.TT);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) h[j] = __vminu2(h[j] - m, a.TT);
+    }
+    uint32_t up = __shfl_up_sync(FULL, h[7], 1, a.G);
+    uint32_t dn = __shfl_down_sync(FULL, h[0], 1, a.G);
+    if (lane_g == 0) up = a.TT;
+    if (lane_g == a.G - 1) dn = a.TT;
+    const uint32_t prev0 = prmt(up, h[7], 0x5432);  // (d0-1, d0+7)
+    const uint32_t next7 = prmt(h[0], dn, 0x5432);  // (d0+8, d0+16)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t pv = j == 0 ? prev0 : h[j - 1];
+        const uint32_t nx = j == 7 ? next7 : h[j + 1];
+        out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[j]));
+        if (PAD) out[j] &= ~padm[j];
+    }
+}
+
+template <bool PAD>
+__device__ __forceinline__ uint32_t wta_key(const uint32_t tot[8], int d0, int L, int G)
+{
+    uint32_t best = 0xFFFFFFFFu;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t lo = tot[j] & 0xFFFFu, hi = tot[j] >> 16;
+        if (!PAD || d0 + j < L) best = min(best, (lo << 9) | (uint32_t)(d0 + j));
+        if (!PAD || d0 + j + 8 < L) best = min(best, (hi << 9) | (uint32_t)(d0 + j + 8));
+    }
+    for (int s = G >> 1; s > 0; s >>= 1) best = min(best, __shfl_xor_sync(FULL, best, s, G));
+    return best & 511u;
+}
+
+template <bool PAD, bool SIGNED>
+__global__ void __launch_bounds__(256, 4) k_final_fast(FastArgs a, const uint8_t *__restrict__ D)
+{
+    const uint32_t t = blockIdx.x * blockDim.x + threadIdx.x;
+    const int b = blockIdx.y;
+    const int lane_g = threadIdx.x & (a.G - 1);
+    const uint32_t pix = t >> a.log2G;
+    bool active = pix < a.npix;
+    if (__all_sync(FULL, !active)) return;
+    const uint32_t cA = a.colour, cB = a.colour ^ 1u;
+    const uint32_t y = a.magic ? __umulhi(pix, a.magic) : pix / (uint32_t)a.Wc;
+    const uint32_t i = pix - y * (uint32_t)a.Wc;
+    const uint32_t o = (cB + y) & 1u;
+    const int x = 2 * (int)i + (int)o;
+    active = active && x < a.W;
+    const bool io = active && lane_g < a.nch;
+    const int d0 = lane_g * CH;
+    const uint32_t P = a.plane;
+    const uint32_t rowstep = (uint32_t)a.Wc * (uint32_t)a.Lp;
+    const uint32_t r = (y * (uint32_t)a.Wc + i) * (uint32_t)a.Lp + (uint32_t)d0;
+    const uint8_t *Mb = a.M + (size_t)b * a.pairM;
+    const uint8_t *MB = Mb + (size_t)(cB * 4u) * P;  // colour-B senders: the incoming of every A pixel
+    const uint8_t *Db = D + (size_t)b * a.pairD;
+
+    uint32_t padm[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        padm[j] = !PAD ? 0u
+                       : (d0 + j >= a.L ? (SIGNED ? 0x00007FFFu : 0x0000FFFFu) : 0u) |
+                             (d0 + j + 8 >= a.L ? (SIGNED ? 0x7FFF0000u : 0xFFFF0000u) : 0u);
+    uint32_t bel[8];
+    {
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (io) w = __ldg(reinterpret_cast<const uint4 *>(Db + cB * P + r));
+        unpack_u8(w, bel);
+    }
+#pragma unroll 1
+    for (int k = 0; k < 4; ++k) {
+        const bool has = k == 0 ? y > 0 : k == 1 ? (int)y < a.H - 1 : k == 2 ? x > 0 : x < a.W - 1;
+        if (__all_sync(FULL, !has)) continue;
+        // neighbour q (colour A) and the direction kk from q to p
+        const int xq = x + (k == 2 ? -1 : (k == 3 ? 1 : 0));
+        const int yq = (int)y + (k == 0 ? -1 : (k == 1 ? 1 : 0));
+        const uint32_t oq = (cA + (uint32_t)yq) & 1u;
+        const uint32_t iq = (uint32_t)(xq - (int)oq) >> 1;
+        const uint32_t rq = ((uint32_t)yq * (uint32_t)a.Wc + iq) * (uint32_t)a.Lp + (uint32_t)d0;
+        const int kk = k ^ 1;
+        const bool hq[4] = {yq > 0, yq < a.H - 1, xq > 0, xq < a.W - 1};
+        const bool ld = io && has;
+        uint4 wi[4], wd = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) wi[k2] = make_uint4(0u, 0u, 0u, 0u);
+        // the incoming of q (its neighbour in direction k2 sends on slot k2^1); q's
+        // incoming from p itself (k2 == kk) is loaded only for q's WTA below
+        const bool wq = k == 3 || (k == 2 && xq == 0);  // this group labels q
+        if (ld && hq[0] && (kk != 0 || wq)) wi[0] = __ldg(reinterpret_cast<const uint4 *>(MB + (1u * P + rq - rowstep)));
+        if (ld && hq[1] && (kk != 1 || wq)) wi[1] = __ldg(reinterpret_cast<const uint4 *>(MB + (rq + rowstep)));
+        if (ld && hq[2] && (kk != 2 || wq)) wi[2] = __ldg(reinterpret_cast<const uint4 *>(MB + (3u * P + rq + (oq - 1u) * (uint32_t)a.Lp)));
+        if (ld && hq[3] && (kk != 3 || wq)) wi[3] = __ldg(reinterpret_cast<const uint4 *>(MB + (2u * P + rq + oq * (uint32_t)a.Lp)));
+        if (ld) wd = __ldg(reinterpret_cast<const uint4 *>(Db + cA * P + rq));
+        uint32_t dq[8], in[4][8];
+        unpack_u8(wd, dq);
+#pragma unroll
+        for (int k2 = 0; k2 < 4; ++k2) unpack_u8(wi[k2], in[k2]);
+        // h_q without p's message: sum the three other directions
+        uint32_t h[8], pin[8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t all4 = iadd3(dq[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+            pin[j] = kk == 0 ? in[0][j] : kk == 1 ? in[1][j] : kk == 2 ? in[2][j] : in[3][j];
+            h[j] = all4 - pin[j];
+        }
+        if (__any_sync(FULL, wq && has)) {
+            // label q: belief D_q + all four incoming = h + p's message
+            uint32_t tot[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tot[j] = h[j] + pin[j];
+            const uint32_t lab = wta_key<PAD>(tot, d0, a.L, a.G);
+            if (wq && has && active && lane_g == 0) a.disp[((size_t)b * a.H + yq) * a.W + xq] = (int32_t)lab;
+        }
+        if (PAD) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) h[j] |= padm[j];
+        }
+        uint32_t m[8];
+        one_message<PAD, SIGNED>(a, h, padm, lane_g, m);
+        if (has) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bel[j] += m[j];
+        }
+    }
+    const uint32_t lab = wta_key<PAD>(bel, d0, a.L, a.G);
+    if (active && lane_g == 0) a.disp[((size_t)b * a.H + y) * a.W + x] = (int32_t)lab;
+}
+
+cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st)
+{
+    const long threads = (long)a.npix * a.G;
+    dim3 grid((unsigned)((threads + 255) / 256), (unsigned)B);
+    const bool pad = (a.L % CH) != 0 || a.G != a.nch;
+    const uint8_t *d = (const uint8_t *)D;
+    if (pad) {
+        if (sgn) k_final_fast<true, true><<<grid, 256, 0, st>>>(a, d);
+        else k_final_fast<true, false><<<grid, 256, 0, st>>>(a, d);
+    } else {
+        if (sgn) k_final_fast<false, true><<<grid, 256, 0, st>>>(a, d);
+        else k_final_fast<false, false><<<grid, 256, 0, st>>>(a, d);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
                                cudaStream_t st)
 {

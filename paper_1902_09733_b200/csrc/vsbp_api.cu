@@ -18,6 +18,8 @@ struct vsbp_bp {
     int Lp, nch, G, log2G;
     int msg_bytes_opt, msg_bytes, kernel;
     int dimg;  // level-0 data term computed from the images inside the update (no D_0 traffic)
+    int final_fuse;  // VSBP_OPT_FINAL: last level-0 iteration fused with the WTA (messages not stored)
+    int final_ran;   // the last call fused it: level-0 messages of the last colour are stale
     int Wl[16], Hl[16], Wcl[16];
     int dbytes[16];
     // workspace plan (bytes) for ws_batch pairs
@@ -115,6 +117,12 @@ bool use_fast(const vsbp_bp *c, int l)
 
 // level 0 of the packed kernel computes its data term from the grey images
 bool use_dimg(const vsbp_bp *c) { return c->dimg && use_fast(c, 0) && c->dbytes[0] == 1 && c->tau_d <= 255; }
+// k_final_fast: packed level-0 update with u8 costs read from memory, a normal
+// (MODE 0) last iteration, and a left neighbour for every colour-A pixel but x = 0
+bool use_final(const vsbp_bp *c)
+{
+    return c->final_fuse && use_fast(c, 0) && !use_dimg(c) && c->dbytes[0] == 1 && c->iters >= 2 && c->W >= 2;
+}
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
 bool fast_signed(const vsbp_bp *c, int l)
@@ -242,6 +250,8 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
     }
     c->msg_bytes = bytes_for_max(c->tau_q);
     c->dimg = 0;  // measured slower (ALU-bound): DESIGN.md §12
+    c->final_fuse = 0;  // measured slower (4x the unpack/sum work per colour-A pixel): DESIGN.md §12
+    c->final_ran = 0;
     *out = c;
     return VSBP_OK;
 }
@@ -267,6 +277,11 @@ int bp_set_option(vsbp_bp *c, int option, int value)
     if (option == VSBP_OPT_DIMG) {
         if (value < 0 || value > 1) return VSBP_EINVAL;
         c->dimg = value;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_FINAL) {
+        if (value < 0 || value > 1) return VSBP_EINVAL;
+        c->final_fuse = value;
         return VSBP_OK;
     }
     return VSBP_EINVAL;
@@ -393,6 +408,18 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 vsbp::FastArgs fa = fast_args(c, l, ws, disp);
                 fa.colour = (uint32_t)(t & 1);
                 const bool wta = (l == 0 && t == c->iters - 1);  // a5 fused for this colour
+                if (wta && use_final(c)) {
+                    // last iteration + WTA of both colours, messages not stored
+                    CK(vsbp::launch_final_fast(D, fa, B, fast_signed(c, l), st));
+                    long long nA = 0, nB = 0;
+                    for (int y = 0; y < g.H; ++y) {
+                        nA += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;
+                        nB += (g.W + (((t + 1 + y) & 1) ? 0 : 1)) / 2;
+                    }
+                    bytes += (double)B * (nA * (double)c->L * c->dbytes[l] +
+                                          nB * ((double)c->L * c->dbytes[l] + 4.0 * c->L * c->msg_bytes));
+                    continue;
+                }
                 int db = c->dbytes[l];
                 if (l == 0 && use_dimg(c)) {  // data term from the images, no D_0 read
                     db = 0;
@@ -417,7 +444,8 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         }
     }
     // a5 (the colour updated last was labelled inside its update when the fast kernel ran)
-    {
+    c->final_ran = use_final(c);
+    if (!c->final_ran) {
         if (use_fast(c, 0)) {
             vsbp::FastArgs fa = fast_args(c, 0, ws, disp);
             fa.colour = (uint32_t)(((c->iters - 1) & 1) ^ 1);  // the colour not updated last
@@ -448,6 +476,7 @@ int bp_disparity(vsbp_bp *c, const uint8_t *left, const uint8_t *right, int32_t 
 int bp_get_messages(vsbp_bp *c, int pair, int level, int32_t *out, void *stream)
 {
     if (!c || !out || level < 0 || level >= c->levels || pair < 0) return VSBP_EINVAL;
+    if (level == 0 && c->final_ran) return VSBP_EINVAL;  // not materialised (VSBP_OPT_FINAL)
     if (!c->ws || pair >= c->ws_batch) return VSBP_EDIM;
     plan(c, c->ws_batch);
     vsbp::Geom g = geom(c, c->ws_batch, level);

@@ -56,6 +56,8 @@ struct FastArgs {
 // dbytes 1 / 2: D is u8 / u16; dbytes 0: level 0 computed from a.gl / a.gr (ImgD)
 cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
                                cudaStream_t st);
+// fused last level-0 iteration + WTA of both colours (a.colour = the colour updated last)
+cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 

@@ -22,21 +22,26 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
 
 
-def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, batch=None):
+def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, batch=None, final=0):
     left = np.asarray(left)
     right = np.asarray(right)
     if left.ndim == 2:
         left, right = left[None], right[None]
     B, H, W = left.shape
-    bp = P.StereoBP(W, H, L, levels, iters, lam, dt, st, batch=batch or B, msg_bytes=msg_bytes, device=dev())
+    bp = P.StereoBP(W, H, L, levels, iters, lam, dt, st, batch=batch or B, msg_bytes=msg_bytes, device=dev(),
+                    final=final)
     disp = bp.disparity(to_dev(left), to_dev(right))
     torch.cuda.synchronize()
     return bp, disp.cpu().numpy()
 
 
 def check_bp_case(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, all_levels=True):
+    """Disparities with the fused final iteration (VSBP_OPT_FINAL) and with the
+    default stored-message path, whose messages are compared on every level."""
+    _, disp_f = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, final=1)
     bp, disp = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes)
     d_o, msgs_o = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
+    assert np.array_equal(disp_f[0], d_o), "disparity differs (fused final iteration)"
     assert np.array_equal(disp[0], d_o), "disparity differs"
     levels_to_check = range(levels) if all_levels else [0]
     q = oracle.quantize(lam, dt, st)
@@ -110,6 +115,8 @@ def test_level0_data_term_from_images_or_memory(W, H, L, levels, dimg):
     r = rng.integers(0, 256, size=(3, H, W), dtype=np.uint8)
     bp = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg)
     disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+    disp_f = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg, final=1).disparity(to_dev(l), to_dev(r))
+    assert np.array_equal(disp_f.cpu().numpy(), disp)
     for b in range(3):
         d_o, msgs_o = oracle.bp_disparity(l[b], r[b], L, levels, 5, return_messages=True)
         assert np.array_equal(disp[b], d_o)
@@ -127,6 +134,8 @@ def test_generic_and_fused_kernels_agree_with_oracle(W, H, L, levels):
     r = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
     d_o, msgs_o = oracle.bp_disparity(l, r, L, levels, 5, return_messages=True)
     D = oracle.cost_volume(l, r, L, oracle.quantize(0.07, 15.0, 1.7))
+    assert np.array_equal(P.StereoBP(W, H, L, levels, 5, device=dev(), final=1).disparity(to_dev(l), to_dev(r))
+                          .cpu().numpy(), d_o)  # fused final iteration
     for kernel in (0, 1):
         bp = P.StereoBP(W, H, L, levels, 5, kernel=kernel, device=dev())
         disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
@@ -144,6 +153,8 @@ def test_batch_equals_single():
     left = np.stack([p[0] for p in pairs])
     right = np.stack([p[1] for p in pairs])
     bp, disp = run_gpu_bp(left, right, 16, 3, 5)
+    _, disp_f = run_gpu_bp(left, right, 16, 3, 5, final=1)
+    assert np.array_equal(disp_f, disp)
     for i in range(3):
         assert np.array_equal(disp[i], oracle.bp_disparity(left[i], right[i], 16, 3, 5))
         _, msgs = oracle.bp_disparity(left[i], right[i], 16, 3, 5, return_messages=True)
@@ -626,3 +637,28 @@ def test_config4_pipeline_jbu_s2_r3():
     disp_o, hi_o, _, _ = oracle.pipeline_pair(left, right, 2, 128, 6, 8, Qo)
     assert np.array_equal(pipe.disp[0].cpu().numpy(), disp_o)
     assert np.max(np.abs(pipe.disp_hi[0].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
+
+
+# ----------------------------------------------------------------------------- a4+a5 fused final iteration
+@pytest.mark.parametrize("W,H,L,levels,iters", [(2, 1, 16, 1, 2), (3, 5, 16, 1, 3), (2, 9, 48, 2, 4), (17, 1, 32, 1, 5),
+                                                (31, 23, 48, 3, 2), (64, 48, 64, 4, 5), (65, 33, 128, 5, 6),
+                                                (40, 31, 64, 3, 8)])
+def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters):
+    """VSBP_OPT_FINAL=1: the last level-0 iteration's messages go straight
+    into the receivers' beliefs.  Disparities equal the oracle and the stored-message
+    path for both parities of the last colour, odd widths, 1-row images, padded label
+    chunks (L = 48) and G = 8 lanes (L = 128); level-0 messages are then not exported."""
+    rng = np.random.default_rng(7 * W + H + L + iters)
+    l = rng.integers(0, 256, size=(2, H, W), dtype=np.uint8)
+    r = np.roll(l, 3, axis=2)
+    r = np.clip(r.astype(np.int32) + rng.integers(-6, 7, size=r.shape), 0, 255).astype(np.uint8)
+    bp = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=1)
+    disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
+    ref = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev()).disparity(to_dev(l), to_dev(r))
+    assert np.array_equal(disp, ref.cpu().numpy())
+    for b in range(2):
+        assert np.array_equal(disp[b], oracle.bp_disparity(l[b], r[b], L, levels, iters))
+    with pytest.raises(RuntimeError, match="EINVAL"):
+        bp.messages(0, 0)
+    if levels > 1:
+        bp.messages(0, 1)  # coarser levels are still materialised
