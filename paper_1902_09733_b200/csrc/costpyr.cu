@@ -19,7 +19,10 @@
 
 namespace vsbp {
 
-constexpr int CP_T = 16;  // level-0 tile side (levels 0..4 of a tile nest inside it)
+constexpr int CP_T = 16;
+#ifndef VSBP_CP_MINB
+#define VSBP_CP_MINB 4  // resident CTAs per SM of k_costpyr_fast
+#endif  // level-0 tile side (levels 0..4 of a tile nest inside it)
 
 __device__ __forceinline__ void store_chunk(void *base, int bytes, size_t off, const int v[CH])
 {
@@ -199,7 +202,7 @@ __device__ __forceinline__ uint32_t d_off32(int c, int y, int i, int H, int Wc, 
 
 // NCH_T > 0: the chunk count is a compile-time power of two (shifts instead of divides)
 template <bool PAD, int NCH_T>
-__global__ void __launch_bounds__(256) k_costpyr_fast(const uint8_t *__restrict__ left,
+__global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_t *__restrict__ left,
                                                       const uint8_t *__restrict__ right, CostPyrArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];

@@ -64,6 +64,23 @@ def main():
     bp = P.StereoBP(676, 380, 64, 5, 5, batch=B, device=dev)
     out = torch.empty((B, 380, 676), dtype=torch.int32, device=dev)
     res["a1_a5_full_bp"] = {"ms_per_pair": timed(lambda: bp.disparity(gl, gr, out=out)) / B}
+    # C4 (BASELINE configs[3]): 1352x760 (2.7K/2), L=128, 6 levels x 8 iterations,
+    # guided upsampling s=2 (r=3, sigma_s=7.5 low-res px) to 2.7K + reprojection
+    B4 = max(1, B // 4)
+    gl2 = P.prep_downsample(L[:B4], 2)
+    gr2 = P.prep_downsample(R[:B4], 2)
+    bp4 = P.StereoBP(1352, 760, 128, 6, 8, batch=B4, device=dev)
+    out4 = torch.empty((B4, 760, 1352), dtype=torch.int32, device=dev)
+    ms_bp4 = timed(lambda: bp4.disparity(gl2, gr2, out=out4), reps=5) / B4
+    I = synthgen.INTRINSICS
+    Q4 = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    o4 = P.jbu_reproject(out4, L[:B4], 2, 7.5, 15.0, 3, Q4)
+    ms_jbu4 = timed(lambda: P.jbu_reproject(out4, L[:B4], 2, 7.5, 15.0, 3, Q4, disp_hi=o4[0], xyz=o4[1],
+                                            n_valid=o4[2]), reps=5) / B4
+    res["c4_bp_1352x760_L128_6x8"] = {"ms_per_pair": ms_bp4, "pairs_per_s": 1e3 / ms_bp4,
+                                       "workspace_MB_per_pair": bp4.workspace.numel() / B4 / 1e6}
+    res["c4_jbu_s2_r3_reproject"] = {"ms_per_pair": ms_jbu4}
+    del bp4, out4, o4
     for k0 in (1, 2, 4):
         cs = P.ConstantSpaceBP(676, 380, 64, 5, 5, k0, batch=B, device=dev)
         res[f"f2_csbp_k0_{k0}"] = {"ms_per_pair": timed(lambda: cs.disparity(gl, gr, out=out)) / B,

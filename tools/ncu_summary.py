@@ -145,7 +145,10 @@ def main():
     if a.traffic_json:
         import json
         with open(a.traffic_json, "w") as f:
-            json.dump({"batch": a.batch, "source": a.out, "dram_bytes_per_launch": traffic}, f, indent=1)
+            # bench.py reports the level-0 message update's traffic (its roofline kernel)
+            dom = next((k for k in traffic if k.startswith("k_update_fast<unsigned char, 0,")), None)
+            json.dump({"batch": a.batch, "source": a.out, "dram_bytes_per_launch": traffic, "dominant": dom}, f,
+                      indent=1)
     with open(a.out, "w") as f:
         f.write("\n".join(parts))
     print(open(a.out).read())
