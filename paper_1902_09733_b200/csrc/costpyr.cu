@@ -21,7 +21,7 @@ namespace vsbp {
 
 constexpr int CP_T = 16;
 #ifndef VSBP_CP_MINB
-#define VSBP_CP_MINB 4  // resident CTAs per SM of k_costpyr_fast
+#define VSBP_CP_MINB 5  // resident CTAs per SM of k_costpyr_fast (48 registers; 4: 6864, 5: 6878, 6: 6875 pairs/s)
 #endif  // level-0 tile side (levels 0..4 of a tile nest inside it)
 
 __device__ __forceinline__ void store_chunk(void *base, int bytes, size_t off, const int v[CH])
