@@ -66,6 +66,51 @@ __global__ void __launch_bounds__(256) k_prep_w(const uint8_t *__restrict__ rgb,
     gray[t] = (uint8_t)((sum + s * s / 2) / (s * s));
 }
 
+// s == 4 with 16-byte aligned footprint rows (W_hi % 16 == 0, 16-byte aligned
+// frames): a thread makes 4 adjacent output pixels of one row from 3 x 16-byte loads
+// per footprint row (12 loads in flight per thread) and stores them as one word.
+// Same arithmetic as k_prep.
+__device__ __forceinline__ int grey_px(uint32_t w0, uint32_t w1, uint32_t w2, int k)
+{
+    // pixel k (0..3) of the 12 bytes w0 w1 w2: bytes 3k, 3k+1, 3k+2
+    const uint32_t lo = k == 0 ? w0 : k == 1 ? __funnelshift_r(w0, w1, 24) : k == 2 ? __funnelshift_r(w1, w2, 16) : w2 >> 8;
+    const int R = lo & 0xff, G = (lo >> 8) & 0xff, Bc = (lo >> 16) & 0xff;
+    return (77 * R + 150 * G + 29 * Bc + 128) >> 8;
+}
+
+__global__ void __launch_bounds__(256) k_prep_v4(const uint8_t *__restrict__ rgb, int W_hi, int H_hi, int n,
+                                                 uint8_t *__restrict__ gray)
+{
+    const int W = W_hi / 4, H = H_hi / 4, Wq = W / 4;
+    const long t = (long)blockIdx.x * blockDim.x + threadIdx.x;
+    if (t >= (long)n * Wq * H) return;
+    const int f = (int)(t / ((long)Wq * H));
+    const long r = t - (long)f * Wq * H;
+    const int Y = (int)(r / Wq), xq = (int)(r - (long)Y * Wq);
+    const uint8_t *base = rgb + (size_t)f * H_hi * W_hi * 3 + (size_t)xq * 48;
+    uint4 v[4][3];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+        const uint4 *row = reinterpret_cast<const uint4 *>(base + (size_t)(Y * 4 + j) * W_hi * 3);
+#pragma unroll
+        for (int q = 0; q < 3; ++q) v[j][q] = __ldg(row + q);
+    }
+    uint32_t out = 0;
+#pragma unroll
+    for (int o = 0; o < 4; ++o) {  // output pixel o: input pixels 4o .. 4o+3 of each row (bytes 12o .. 12o+11)
+        int sum = 0;
+#pragma unroll
+        for (int j = 0; j < 4; ++j) {
+            const uint32_t w[12] = {v[j][0].x, v[j][0].y, v[j][0].z, v[j][0].w, v[j][1].x, v[j][1].y,
+                                    v[j][1].z, v[j][1].w, v[j][2].x, v[j][2].y, v[j][2].z, v[j][2].w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) sum += grey_px(w[3 * o], w[3 * o + 1], w[3 * o + 2], k);
+        }
+        out |= (uint32_t)((sum + 8) / 16) << (8 * o);
+    }
+    *reinterpret_cast<uint32_t *>(gray + ((size_t)f * H + Y) * W + (size_t)xq * 4) = out;
+}
+
 // ======================================================================== a7
 struct QMat {
     float q[16];
@@ -164,7 +209,10 @@ cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, ui
 {
     const long threads = (long)n * (W_hi / s) * (H_hi / s);
     const unsigned nb = (unsigned)((threads + 255) / 256);
-    if (s == 4 && ((uintptr_t)rgb & 3) == 0)
+    if (s == 4 && W_hi % 16 == 0 && ((uintptr_t)rgb & 15) == 0 && ((uintptr_t)gray & 3) == 0) {
+        const long tq = (long)n * (W_hi / 16) * (H_hi / 4);
+        k_prep_v4<<<(unsigned)((tq + 255) / 256), 256, 0, st>>>(rgb, W_hi, H_hi, n, gray);
+    } else if (s == 4 && ((uintptr_t)rgb & 3) == 0)
         k_prep_w<1><<<nb, 256, 0, st>>>(rgb, W_hi, H_hi, n, gray);
     else if (s == 8 && ((uintptr_t)rgb & 3) == 0)
         k_prep_w<2><<<nb, 256, 0, st>>>(rgb, W_hi, H_hi, n, gray);

@@ -198,6 +198,19 @@ def test_prep_bit_exact(s):
     assert np.array_equal(g, oracle.prep(rgb, s))
 
 
+@pytest.mark.parametrize("W,H,off", [(160, 76, 0), (160, 76, 4), (160, 76, 1), (64, 4, 0), (208, 36, 0)])
+def test_prep_s4_kernels(W, H, off):
+    """s = 4 runs a 4-pixels-per-thread kernel on 16-byte aligned rows (W % 16 == 0),
+    the word kernel on 4-byte alignment and the generic one otherwise (off = byte
+    offset of the frame in its buffer)."""
+    frames = np.stack([synthgen.value_noise_rgb(40 + i + W, W, H) for i in range(3)])
+    buf = torch.zeros(frames.size + off, dtype=torch.uint8, device=dev())
+    buf[off:] = to_dev(frames.reshape(-1))
+    g = P.prep_downsample(buf[off:].view(3, H, W, 3), 4).cpu().numpy()
+    for i in range(3):
+        assert np.array_equal(g[i], oracle.prep(frames[i], 4))
+
+
 def test_prep_full_frame_batch():
     frames = np.stack([synthgen.value_noise_rgb(30 + i, 2704, 1520) for i in range(2)])
     g = P.prep_downsample(to_dev(frames), 4).cpu().numpy()
