@@ -82,15 +82,17 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        D_0.  Results are identical; 1 trades 11 % of the level-0
  *                        bytes for ~10 % more ALU work and measured slower. */
 #define VSBP_OPT_DIMG 3
-/*   VSBP_OPT_FINAL     : 1 = the last level-0 iteration is fused with the WTA of
- *                        both colours (k_final_fast): its messages go straight into
- *                        the receivers' beliefs and are never stored, so
+/*   VSBP_OPT_FINAL     : 1 or 2 = the last level-0 iteration is fused with the WTA
+ *                        of both colours: its messages go straight into the
+ *                        receivers' beliefs and are never stored, so
  *                        bp_get_messages(level 0) returns VSBP_EINVAL after such a
- *                        call; 0 (default) = store them and label in separate passes.
- *                        Disparities are identical; 1 moves 57 % fewer bytes but
- *                        recomputes each colour-A pixel's belief for each of its four
- *                        receivers and measured slower.  Applies when the packed
- *                        kernels run with u8 level-0 costs, iters >= 2 and W >= 2. */
+ *                        call.  1: each colour-B pixel recomputes its neighbours'
+ *                        messages (k_final_fast); 2: tiles keep the messages in
+ *                        shared memory (k_final_tile).  0 (default) = store them and
+ *                        label in separate passes.  Disparities are identical; both
+ *                        fused variants move fewer bytes but measured slower
+ *                        (DESIGN.md §12).  Applies when the packed kernels run with
+ *                        u8 level-0 costs, iters >= 2 and W >= 2. */
 #define VSBP_OPT_FINAL 4
 int bp_set_option(vsbp_bp *ctx, int option, int value);
 

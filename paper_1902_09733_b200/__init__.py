@@ -141,7 +141,7 @@ class StereoBP:
     device workspace (a torch uint8 tensor) for up to ``batch`` pairs."""
 
     def __init__(self, W, H, ndisp, levels, iters, lam=0.07, data_trunc=15.0, disc_trunc=1.7, batch=1,
-                 msg_bytes=0, kernel=0, device="cuda", dimg=0, final=0):
+                 msg_bytes=0, kernel=0, device="cuda", dimg=0, final=None):
         self._h = C.c_void_p()
         _check(lib().bp_create(W, H, ndisp, levels, iters, lam, data_trunc, disc_trunc, C.byref(self._h)),
                "bp_create")
@@ -151,8 +151,10 @@ class StereoBP:
             _check(lib().bp_set_option(self._h, VSBP_OPT_KERNEL, kernel), "bp_set_option")
         if dimg:
             _check(lib().bp_set_option(self._h, VSBP_OPT_DIMG, 1), "bp_set_option")
+        if final is None:  # experiment knob: VSBP_FINAL in the environment
+            final = int(os.environ.get("VSBP_FINAL", "0"))
         if final:  # fused last level-0 iteration + WTA (level-0 messages not stored)
-            _check(lib().bp_set_option(self._h, VSBP_OPT_FINAL, 1), "bp_set_option")
+            _check(lib().bp_set_option(self._h, VSBP_OPT_FINAL, final), "bp_set_option")
         self.W, self.H, self.L, self.levels, self.iters, self.batch = W, H, ndisp, levels, iters, batch
         nbytes = int(lib().bp_workspace_bytes(self._h, batch))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)

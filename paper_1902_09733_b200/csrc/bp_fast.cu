@@ -434,6 +434,193 @@ __global__ void __launch_bounds__(256, 4) k_final_fast(FastArgs a, const uint8_t
     if (active && lane_g == 0) a.disp[((size_t)b * a.H + y) * a.W + x] = (int32_t)lab;
 }
 
+// ---------------------------------------------------------------- fused final iteration, tiled
+// k_final_tile: the same fusion as k_final_fast without the recomputation.  A CTA
+// owns a tile of TY rows x TX colour-columns of colour-B pixels and the colour-A
+// pixels with the same coordinates.  Phase 1 updates every colour-A pixel adjacent
+// to the tile (the owned ones, the unowned column on the side the row's parity
+// needs, and the rows above and below -- vertical messages only) exactly like
+// k_update_fast, but keeps the packed u8 messages in shared memory; owned pixels
+// are labelled from D + the four incoming.  Phase 2 labels each colour-B pixel of
+// the tile from D_B + its four messages read from shared memory.  HBM per pixel
+// pair ~ (1 + halo) * 5L + L instead of 14L; nothing but labels is written.
+constexpr int FT_TY = 8, FT_TX = 16;
+
+template <bool PAD, bool SIGNED>
+__global__ void __launch_bounds__(256, 3) k_final_tile(FastArgs a, const uint8_t *__restrict__ D)
+{
+    extern __shared__ uint4 fsm[];  // [(TY+2)*(TX+2)][4][nch] packed u8 chunks
+    const int b = blockIdx.z;
+    const int G = a.G, nch = a.nch;
+    const int lane_g = threadIdx.x & (G - 1);
+    const int grp = threadIdx.x >> a.log2G, ngrp = blockDim.x >> a.log2G;
+    const int y0 = blockIdx.y * FT_TY, i0 = blockIdx.x * FT_TX;
+    const uint32_t cA = a.colour, cB = a.colour ^ 1u;
+    const bool io_lane = lane_g < nch;
+    const int d0 = lane_g * CH;
+    const uint32_t P = a.plane;
+    const uint32_t rowstep = (uint32_t)a.Wc * (uint32_t)a.Lp;
+    const uint8_t *Mb = a.M + (size_t)b * a.pairM;
+    const uint8_t *MB = Mb + (size_t)(cB * 4u) * P;
+    const uint8_t *Db = D + (size_t)b * a.pairD;
+    constexpr int NA = (FT_TY + 2) * (FT_TX + 2);
+    uint32_t padm[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        padm[j] = !PAD ? 0u
+                       : (d0 + j >= a.L ? (SIGNED ? 0x00007FFFu : 0x0000FFFFu) : 0u) |
+                             (d0 + j + 8 >= a.L ? (SIGNED ? 0x7FFF0000u : 0xFFFF0000u) : 0u);
+
+    // ---- phase 1: colour-A pixels around the tile (warp-uniform trip count)
+    for (int base = 0; base < NA; base += ngrp) {
+        const int task = base + grp;
+        const int tya = task / (FT_TX + 2), txa = task - tya * (FT_TX + 2);
+        const int ya = y0 - 1 + tya, ia = i0 - 1 + txa;
+        const uint32_t oa = (cA + (uint32_t)ya) & 1u;
+        const int xa = 2 * ia + (int)oa;
+        const bool inimg = task < NA && ya >= 0 && ya < a.H && ia >= 0 && ia < a.Wc && xa < a.W;
+        const bool rowin = tya >= 1 && tya <= FT_TY;
+        // the B pixels of row ya have parity oB = 1 - oa: their A neighbours span
+        // colour-columns [i0 + oB - 1, i0 + TX + oB - 1]
+        const int lo_t = oa ? 0 : 1;  // first needed txa in a tile row
+        const bool need_h = rowin && txa >= lo_t && txa <= lo_t + FT_TX;
+        const bool need_v = txa >= 1 && txa <= FT_TX;  // rows y0-1 .. y0+TY
+        const bool owned = rowin && txa >= 1 && txa <= FT_TX;
+        const bool act = inimg && (need_h || need_v);
+        const bool io = act && io_lane;
+        const uint32_t r = ((uint32_t)ya * (uint32_t)a.Wc + (uint32_t)ia) * (uint32_t)a.Lp + (uint32_t)d0;
+        const bool has[4] = {ya > 0, ya < a.H - 1, xa > 0, xa < a.W - 1};
+        uint4 wi[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) wi[k] = make_uint4(0u, 0u, 0u, 0u);
+        if (io && has[0]) wi[0] = __ldg(reinterpret_cast<const uint4 *>(MB + (1u * P + r - rowstep)));
+        if (io && has[1]) wi[1] = __ldg(reinterpret_cast<const uint4 *>(MB + (r + rowstep)));
+        if (io && has[2]) wi[2] = __ldg(reinterpret_cast<const uint4 *>(MB + (3u * P + r + (oa - 1u) * (uint32_t)a.Lp)));
+        if (io && has[3]) wi[3] = __ldg(reinterpret_cast<const uint4 *>(MB + (2u * P + r + oa * (uint32_t)a.Lp)));
+        uint4 wd = make_uint4(0u, 0u, 0u, 0u);
+        if (io) wd = __ldg(reinterpret_cast<const uint4 *>(Db + cA * P + r));
+        uint32_t dv[8], in[4][8];
+        unpack_u8(wd, dv);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) unpack_u8(wi[k], in[k]);
+        if (__any_sync(FULL, owned && act)) {
+            uint32_t tot[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) tot[j] = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+            const uint32_t lab = wta_key<PAD>(tot, d0, a.L, G);
+            if (owned && inimg && lane_g == 0) a.disp[((size_t)b * a.H + ya) * a.W + xa] = (int32_t)lab;
+        }
+        uint4 *slot = fsm + (size_t)task * 4 * nch + lane_g;
+#pragma unroll
+        for (int kp = 0; kp < 4; kp += 2) {
+            if (!__any_sync(FULL, act && (kp == 0 ? need_v : need_h))) continue;
+            uint32_t h[2][8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t bs = kp == 0 ? iadd3(dv[j], in[2][j], in[3][j]) : iadd3(dv[j], in[0][j], in[1][j]);
+                h[0][j] = bs + in[kp + 1][j];
+                h[1][j] = bs + in[kp][j];
+                if (PAD) {
+                    h[0][j] |= padm[j];
+                    h[1][j] |= padm[j];
+                }
+            }
+            uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
+            for (int s2 = G >> 1; s2 > 0; s2 >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s2, G));
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
+                if (SIGNED) {
+                    const uint32_t neg = prmt(0u - hm, 0u, 0x1010);
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) h[e][j] = (uint32_t)__viaddmin_s16x2(h[e][j], neg, a.TT);
+                } else {
+#pragma unroll
+                    for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
+                }
+            }
+            uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, G);
+            uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, G);
+            if (lane_g == 0) up = a.TT;
+            if (lane_g == G - 1) dn = a.TT;
+#pragma unroll
+            for (int e = 0; e < 2; ++e) {
+                const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);
+                const uint32_t next7 = prmt(h[e][0], dn, e == 0 ? 0x5432 : 0x7632);
+                uint32_t out[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) {
+                    const uint32_t pv = j == 0 ? prev0 : h[e][j - 1];
+                    const uint32_t nx = j == 7 ? next7 : h[e][j + 1];
+                    out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[e][j]));
+                    if (PAD) out[j] &= ~padm[j];
+                }
+                if (io && (kp == 0 ? need_v : need_h)) slot[(kp + e) * nch] = pack_u8(out);
+            }
+        }
+    }
+    __syncthreads();
+
+    // ---- phase 2: colour-B pixels of the tile
+    for (int base = 0; base < FT_TY * FT_TX; base += ngrp) {
+        const int bt = base + grp;
+        const int ty = bt / FT_TX, tx = bt - ty * FT_TX;
+        const int y = y0 + ty, ib = i0 + tx;
+        const uint32_t ob = (cB + (uint32_t)y) & 1u;
+        const int x = 2 * ib + (int)ob;
+        const bool act = bt < FT_TY * FT_TX && y < a.H && ib < a.Wc && x < a.W;
+        const bool io = act && io_lane;
+        const uint32_t r = ((uint32_t)y * (uint32_t)a.Wc + (uint32_t)ib) * (uint32_t)a.Lp + (uint32_t)d0;
+        uint4 wd = make_uint4(0u, 0u, 0u, 0u);
+        if (io) wd = __ldg(reinterpret_cast<const uint4 *>(Db + cB * P + r));
+        uint32_t bel[8];
+        unpack_u8(wd, bel);
+        const bool has[4] = {y > 0, y < a.H - 1, x > 0, x < a.W - 1};
+        // neighbour k's tile slot and the direction it sends toward this pixel
+        const int sl[4] = {ty * (FT_TX + 2) + tx + 1, (ty + 2) * (FT_TX + 2) + tx + 1,
+                           (ty + 1) * (FT_TX + 2) + tx + (int)ob, (ty + 1) * (FT_TX + 2) + tx + (int)ob + 1};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+            if (!(io && has[k])) continue;
+            uint32_t m[8];
+            unpack_u8(fsm[((size_t)sl[k] * 4 + (k ^ 1)) * nch + lane_g], m);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) bel[j] += m[j];
+        }
+        const uint32_t lab = wta_key<PAD>(bel, d0, a.L, G);
+        if (act && lane_g == 0) a.disp[((size_t)b * a.H + y) * a.W + x] = (int32_t)lab;
+    }
+}
+
+size_t final_tile_smem(int nch) { return (size_t)(FT_TY + 2) * (FT_TX + 2) * 4 * nch * sizeof(uint4); }
+
+cudaError_t launch_final_tile(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st)
+{
+    const size_t smem = final_tile_smem(a.nch);
+    const bool pad = (a.L % CH) != 0 || a.G != a.nch;
+    static bool attr = false;
+    if (!attr) {
+        const void *fs[] = {(const void *)k_final_tile<false, false>, (const void *)k_final_tile<false, true>,
+                            (const void *)k_final_tile<true, false>, (const void *)k_final_tile<true, true>};
+        for (const void *f : fs) {
+            cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024);
+            if (e != cudaSuccess) return e;
+        }
+        attr = true;
+    }
+    dim3 grid((unsigned)((a.Wc + FT_TX - 1) / FT_TX), (unsigned)((a.H + FT_TY - 1) / FT_TY), (unsigned)B);
+    const uint8_t *d = (const uint8_t *)D;
+    if (pad) {
+        if (sgn) k_final_tile<true, true><<<grid, 256, smem, st>>>(a, d);
+        else k_final_tile<true, false><<<grid, 256, smem, st>>>(a, d);
+    } else {
+        if (sgn) k_final_tile<false, true><<<grid, 256, smem, st>>>(a, d);
+        else k_final_tile<false, false><<<grid, 256, smem, st>>>(a, d);
+    }
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st)
 {
     const long threads = (long)a.npix * a.G;

@@ -280,7 +280,7 @@ int bp_set_option(vsbp_bp *c, int option, int value)
         return VSBP_OK;
     }
     if (option == VSBP_OPT_FINAL) {
-        if (value < 0 || value > 1) return VSBP_EINVAL;
+        if (value < 0 || value > 2) return VSBP_EINVAL;
         c->final_fuse = value;
         return VSBP_OK;
     }
@@ -410,7 +410,10 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 const bool wta = (l == 0 && t == c->iters - 1);  // a5 fused for this colour
                 if (wta && use_final(c)) {
                     // last iteration + WTA of both colours, messages not stored
-                    CK(vsbp::launch_final_fast(D, fa, B, fast_signed(c, l), st));
+                    if (c->final_fuse == 2)
+                        CK(vsbp::launch_final_tile(D, fa, B, fast_signed(c, l), st));
+                    else
+                        CK(vsbp::launch_final_fast(D, fa, B, fast_signed(c, l), st));
                     long long nA = 0, nB = 0;
                     for (int y = 0; y < g.H; ++y) {
                         nA += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;

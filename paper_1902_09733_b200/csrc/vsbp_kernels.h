@@ -58,6 +58,7 @@ cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int
                                cudaStream_t st);
 // fused last level-0 iteration + WTA of both colours (a.colour = the colour updated last)
 cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);
+cudaError_t launch_final_tile(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);
 cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 

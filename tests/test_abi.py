@@ -86,9 +86,9 @@ def test_level_dims_and_workspace():
     assert L.bp_workspace_bytes(h, 1) > n1
     assert L.bp_set_option(h, P.VSBP_OPT_MSG_BYTES, 3) == -1
     # 0/1 switches; anything else (or an unknown option) is refused
-    for opt in (P.VSBP_OPT_KERNEL, P.VSBP_OPT_DIMG, P.VSBP_OPT_FINAL):
-        assert L.bp_set_option(h, opt, 1) == 0 and L.bp_set_option(h, opt, 0) == 0
-        assert L.bp_set_option(h, opt, 2) == -1
+    for opt, top in ((P.VSBP_OPT_KERNEL, 1), (P.VSBP_OPT_DIMG, 1), (P.VSBP_OPT_FINAL, 2)):
+        assert all(L.bp_set_option(h, opt, v) == 0 for v in range(top + 1))
+        assert L.bp_set_option(h, opt, top + 1) == -1 and L.bp_set_option(h, opt, -1) == -1
     assert L.bp_set_option(h, 99, 0) == -1
     assert L.bp_set_workspace(h, C.c_void_p(256), 10, 1) == -2  # too small
     assert L.bp_disparity_batch(h, 1, C.c_void_p(256), C.c_void_p(256), C.c_void_p(256), None) == -2  # no ws

@@ -38,10 +38,11 @@ def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_byt
 def check_bp_case(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, all_levels=True):
     """Disparities with the fused final iteration (VSBP_OPT_FINAL) and with the
     default stored-message path, whose messages are compared on every level."""
-    _, disp_f = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, final=1)
     bp, disp = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes)
     d_o, msgs_o = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
-    assert np.array_equal(disp_f[0], d_o), "disparity differs (fused final iteration)"
+    for variant in (1, 2):
+        _, disp_f = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, final=variant)
+        assert np.array_equal(disp_f[0], d_o), f"disparity differs (fused final iteration, variant {variant})"
     assert np.array_equal(disp[0], d_o), "disparity differs"
     levels_to_check = range(levels) if all_levels else [0]
     q = oracle.quantize(lam, dt, st)
@@ -115,7 +116,7 @@ def test_level0_data_term_from_images_or_memory(W, H, L, levels, dimg):
     r = rng.integers(0, 256, size=(3, H, W), dtype=np.uint8)
     bp = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg)
     disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
-    disp_f = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg, final=1).disparity(to_dev(l), to_dev(r))
+    disp_f = P.StereoBP(W, H, L, levels, 5, batch=3, device=dev(), dimg=dimg, final=2).disparity(to_dev(l), to_dev(r))
     assert np.array_equal(disp_f.cpu().numpy(), disp)
     for b in range(3):
         d_o, msgs_o = oracle.bp_disparity(l[b], r[b], L, levels, 5, return_messages=True)
@@ -153,7 +154,7 @@ def test_batch_equals_single():
     left = np.stack([p[0] for p in pairs])
     right = np.stack([p[1] for p in pairs])
     bp, disp = run_gpu_bp(left, right, 16, 3, 5)
-    _, disp_f = run_gpu_bp(left, right, 16, 3, 5, final=1)
+    _, disp_f = run_gpu_bp(left, right, 16, 3, 5, final=2)
     assert np.array_equal(disp_f, disp)
     for i in range(3):
         assert np.array_equal(disp[i], oracle.bp_disparity(left[i], right[i], 16, 3, 5))
@@ -656,7 +657,8 @@ def test_config4_pipeline_jbu_s2_r3():
 @pytest.mark.parametrize("W,H,L,levels,iters", [(2, 1, 16, 1, 2), (3, 5, 16, 1, 3), (2, 9, 48, 2, 4), (17, 1, 32, 1, 5),
                                                 (31, 23, 48, 3, 2), (64, 48, 64, 4, 5), (65, 33, 128, 5, 6),
                                                 (40, 31, 64, 3, 8)])
-def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters):
+@pytest.mark.parametrize("variant", [1, 2])
+def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters, variant):
     """VSBP_OPT_FINAL=1: the last level-0 iteration's messages go straight
     into the receivers' beliefs.  Disparities equal the oracle and the stored-message
     path for both parities of the last colour, odd widths, 1-row images, padded label
@@ -665,9 +667,9 @@ def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters):
     l = rng.integers(0, 256, size=(2, H, W), dtype=np.uint8)
     r = np.roll(l, 3, axis=2)
     r = np.clip(r.astype(np.int32) + rng.integers(-6, 7, size=r.shape), 0, 255).astype(np.uint8)
-    bp = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=1)
+    bp = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=variant)
     disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
-    ref = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev()).disparity(to_dev(l), to_dev(r))
+    ref = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=0).disparity(to_dev(l), to_dev(r))
     assert np.array_equal(disp, ref.cpu().numpy())
     for b in range(2):
         assert np.array_equal(disp[b], oracle.bp_disparity(l[b], r[b], L, levels, iters))
