@@ -500,6 +500,11 @@ class StereoPipeline:
     def run(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, first_pair_id: int = 0, stream=None):
         """left_rgb, right_rgb: uint8 [B,H_hi,W_hi,3] on the device.  Returns the
         per-pair summary tensor (device); disp / disp_hi / xyz stay in the object."""
+        guide = self.run_bp(left_rgb, right_rgb, stream)
+        return self.run_jbu(guide, first_pair_id, stream)
+
+    def run_bp(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, stream=None) -> torch.Tensor:
+        """a0-a5 (and f1/f3 when configured); returns the JBU guide for run_jbu."""
         B = left_rgb.shape[0]
         if self.camera is not None:
             rectify_prep(left_rgb, self.camera, self.s, gray=self.gray[0, :B], rect=self.rect[:B], stream=stream)
@@ -517,6 +522,11 @@ class StereoPipeline:
             self.corners = xy
             self.matches = zssd_match(self.gray[0, :B], self.gray[1, :B], xy, f.get("r", 5), f.get("sr", 16),
                                       f.get("max_cost", 2 ** 62), stream=stream)
+        return guide
+
+    def run_jbu(self, guide: torch.Tensor, first_pair_id: int = 0, stream=None) -> torch.Tensor:
+        """a6-a8 on the labels of the last run_bp; returns the per-pair summary."""
+        B = guide.shape[0]
         jbu_reproject(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
                       self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
                       stream=stream)
