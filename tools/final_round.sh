@@ -14,7 +14,7 @@ timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TA
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 timeout 900 python tools/bench_rows.py --out gpurun_out/rows_$TAG.json > /dev/null 2> gpurun_out/rows_$TAG.err; echo "rows rc=$?"
 timeout 300 python tools/time_icp.py > gpurun_out/icp_$TAG.json 2>&1; echo "icp rc=$?"
-ARGS="--batch 32 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pool 1"
+ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pool 1"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
 for cap in k_update_fast:21 k_jbu_vec:1 k_costpyr_fast:1; do
