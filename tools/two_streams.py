@@ -19,7 +19,7 @@ import paper_1902_09733_b200 as P  # noqa: E402
 
 def main():
     dev = torch.device("cuda:0")
-    B = 32
+    B = int(os.environ.get("TS_BATCH", "32"))
     I = bench.q_intrinsics()
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     lpool, rpool = bench.make_pool(7000, 4)
