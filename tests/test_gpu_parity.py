@@ -618,20 +618,24 @@ def test_icp_failure_and_identity():
 
 # ----------------------------------------------------------------------------- bench configuration
 def test_bench_launch_configuration_sampled_pairs():
-    """The configuration bench.py times (C5: 32 pairs per launch, 2.7K RGB, s=4,
-    L=64, 5x5, JBU r=2): two sampled pairs of the batch (first and last, different
-    scenes) through the whole path against the oracle."""
+    """The configuration bench.py times (C5: 128 pairs per launch -- bench.py's
+    default batch --, 2.7K RGB, s=4, L=64, 5x5, JBU r=2): three sampled pairs of the
+    batch (first, middle, last; two different scenes) through the whole path against
+    the oracle."""
     import bench
-    B = 32
+    B = 128
     I = synthgen.INTRINSICS
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(bench.W_HI, bench.H_HI, bench.S_DOWN, bench.NDISP, bench.LEVELS, bench.ITERS, batch=B,
                             Q=Q, device=dev())
     lp, rp = bench.make_pool(7000, 2)
-    idx = [0] * (B - 1) + [1]
-    summ = pipe.run(to_dev(lp[idx]), to_dev(rp[idx]), first_pair_id=5).cpu().numpy()
+    idx = [0] * B
+    idx[B // 2] = idx[B - 1] = 1
+    sel = torch.tensor(idx, device=dev())
+    summ = pipe.run(to_dev(lp)[sel].contiguous(), to_dev(rp)[sel].contiguous(), first_pair_id=5).cpu().numpy()
     Qo = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
-    for b, k in ((0, 0), (B - 1, 1)):
+    for b in (0, B // 2, B - 1):
+        k = idx[b]
         disp_o, hi_o, _, n_o = oracle.pipeline_pair(lp[k], rp[k], bench.S_DOWN, bench.NDISP, bench.LEVELS,
                                                     bench.ITERS, Qo)
         assert np.array_equal(pipe.disp[b].cpu().numpy(), disp_o)
