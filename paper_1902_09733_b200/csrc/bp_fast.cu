@@ -178,19 +178,21 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
         if (io && has[3]) wi[3] = __ldg(reinterpret_cast<const uint4 *>(Mo + (2u * P + r + o * (uint32_t)a.Lp)));
     } else if (MODE == 2) {
         const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
+        // neighbour k's parent (px, py) sends on slot k^1; vertical neighbours share
+        // the pixel's parent column, horizontal ones its parent row
+        const int X = x >> 1, Y = (int)y >> 1;
+        const int pyu = ((int)y - 1) >> 1, pyd = ((int)y + 1) >> 1, pxl = (x - 1) >> 1, pxr = (x + 1) >> 1;
+        const uint32_t Lp = (uint32_t)a.Lp, Wcp = (uint32_t)a.Wcp;
 #pragma unroll
         for (int k = 0; k < 4; ++k) {
-            if (!io || !has[k]) continue;
-            const int qx = x + (k == 2 ? -1 : (k == 3 ? 1 : 0));
-            const int qy = (int)y + (k == 0 ? -1 : (k == 1 ? 1 : 0));
-            const int px = qx >> 1, py = qy >> 1, slot = k ^ 1;
+            const int px = k == 2 ? pxl : (k == 3 ? pxr : X);
+            const int py = k == 0 ? pyu : (k == 1 ? pyd : Y);
+            const int slot = k ^ 1;
             // R-12: the parent's slot toward a missing neighbour counts as 0
             const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
-            if (!ph) continue;
             const uint32_t off = ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
-                                 ((uint32_t)py * (uint32_t)a.Wcp + (uint32_t)(px >> 1)) * (uint32_t)a.Lp +
-                                 (uint32_t)d0;
-            wi[k] = __ldg(reinterpret_cast<const uint4 *>(Mpb + off));
+                                 ((uint32_t)py * Wcp + (uint32_t)(px >> 1)) * Lp + (uint32_t)d0;
+            if (io && has[k] && ph) wi[k] = __ldg(reinterpret_cast<const uint4 *>(Mpb + off));
         }
     }
     uint32_t dv[8];
