@@ -232,6 +232,18 @@ def test_jbu_small(s, r, ss, sr):
     assert np.max(np.abs(got - ref)) <= 1e-4
 
 
+@pytest.mark.parametrize("s,r", [(4, 6), (2, 8), (8, 7)])
+def test_jbu_large_radius_scalar_path(s, r):
+    """Radii above 5 (beyond the paper's 2..5) run on the one-pixel kernel: same
+    tolerance vs the oracle, and still equal to the oracle near the borders."""
+    rng = np.random.default_rng(100 * s + r)
+    lo = rng.integers(0, 256 // s, size=(11, 17)).astype(np.int32)
+    guide = synthgen.value_noise_rgb(s * r, 17 * s, 11 * s)
+    got = P.jbu_upsample(to_dev(lo), to_dev(guide), s, 3.75, 15.0, r).cpu().numpy().astype(np.float64)
+    ref = oracle.jbu(lo, guide, s, 3.75, 15.0, r)
+    assert np.max(np.abs(got - ref)) <= 1e-4
+
+
 def test_jbu_adversarial_colours():
     """Every tap far in colour from the pixel (large |logit|) still within 1e-4."""
     s, r = 4, 2
