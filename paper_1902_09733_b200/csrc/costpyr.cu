@@ -14,6 +14,8 @@
 // colour-split, chunk-packed layout of vsbp_internal.cuh.  The cost volume is
 // never read back from HBM to build the pyramid: HBM traffic is the images plus
 // one write of each fused level.
+#include <stdlib.h>
+
 #include "vsbp_internal.cuh"
 #include "vsbp_kernels.h"
 
@@ -200,26 +202,28 @@ __device__ __forceinline__ uint32_t d_off32(int c, int y, int i, int H, int Wc, 
     return (((uint32_t)c * (uint32_t)H + (uint32_t)y) * (uint32_t)Wc + (uint32_t)i) * (uint32_t)Lp;
 }
 
-// NCH_T > 0: the chunk count is a compile-time power of two (shifts instead of divides)
-template <bool PAD, int NCH_T>
+// NCH_T > 0: the chunk count is a compile-time power of two (shifts instead of divides).
+// TXW: tile width in level-0 pixels (16, or 32 when at most levels 0-1 are fused:
+// two quad-chunks per thread amortise the per-thread setup and the staged window)
+template <bool PAD, int NCH_T, int TXW = CP_T>
 __global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_t *__restrict__ left,
                                                       const uint8_t *__restrict__ right, CostPyrArgs a)
 {
     extern __shared__ __align__(16) unsigned char smem[];
     const int b = blockIdx.z;
-    const int X0 = blockIdx.x * CP_T, Y0 = blockIdx.y * CP_T;
+    const int X0 = blockIdx.x * TXW, Y0 = blockIdx.y * CP_T;
     const int L = a.L, Lp = a.Lp, nch = NCH_T > 0 ? NCH_T : a.nch;
     const int W = a.W[0], H = a.H[0];
-    const int span = Lp + CP_T - 9;        // columns i = X0-Lp+9 .. X0+15
+    const int span = Lp + TXW - 9;         // columns i = X0-Lp+9 .. X0+TXW-1
     const int spanp = (span + 3) & ~3;     // row stride (16-byte rows)
     const int i0 = X0 - Lp + 9;
-    uint8_t *sl = smem;                     // [16][16]
-    uint32_t *sr = reinterpret_cast<uint32_t *>(smem + CP_T * CP_T);  // [16][spanp]: lambda_q (R(i), R(i-8)) as s16x2
+    uint8_t *sl = smem;                     // [16][TXW]
+    uint32_t *sr = reinterpret_cast<uint32_t *>(smem + CP_T * TXW);  // [16][spanp]: lambda_q (R(i), R(i-8)) as s16x2
     int *sD = reinterpret_cast<int *>(smem + a.img_smem);
     const uint8_t *lb = left + (size_t)b * H * W;
     const uint8_t *rb = right + (size_t)b * H * W;
-    for (int e = threadIdx.x; e < CP_T * CP_T; e += blockDim.x) {
-        const int x = X0 + (e & (CP_T - 1)), y = Y0 + e / CP_T;
+    for (int e = threadIdx.x; e < CP_T * TXW; e += blockDim.x) {
+        const int x = X0 + (e & (TXW - 1)), y = Y0 + e / TXW;
         sl[e] = (x < W && y < H) ? __ldg(lb + (size_t)y * W + x) : 0;
     }
     // right rows: one warp per row.  Fast path (W % 4 == 0, 4-byte aligned rows,
@@ -267,12 +271,12 @@ __global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_
 
     const uint32_t lt = (uint32_t)(a.lam_q * a.tau_d);
     const uint32_t T2 = lt | (lt << 16);
-    constexpr int TQ = CP_T / 2;
+    constexpr int TQ = CP_T / 2, TQX = TXW / 2;
     uint8_t *D0 = (uint8_t *)a.D[0] + (size_t)b * a.pairD[0] * a.dbytes[0];
     uint8_t *D1 = a.F > 1 ? (uint8_t *)a.D[1] + (size_t)b * a.pairD[1] * a.dbytes[1] : nullptr;
-    for (int it = threadIdx.x; it < TQ * TQ * nch; it += blockDim.x) {
+    for (int it = threadIdx.x; it < TQX * TQ * nch; it += blockDim.x) {
         const int q = NCH_T > 0 ? it / NCH_T : it / nch, k = it - q * nch;
-        const int qx = q % TQ, qy = q / TQ;
+        const int qx = q % TQX, qy = q / TQX;
         uint32_t mask[8];
 #pragma unroll
         for (int j = 0; j < 8; ++j)
@@ -296,7 +300,7 @@ __global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_
             for (int jx = 0; jx < 2; ++jx) {
                 const int px = 2 * qx + jx, x = X0 + px;
                 if (x >= W) continue;
-                const uint32_t lv = (uint32_t)lam_i * sl[py * CP_T + px];
+                const uint32_t lv = (uint32_t)lam_i * sl[py * TXW + px];
                 const uint32_t lp1 = (lv + 1u) * 0x00010001u;
                 const uint32_t nl2 = ((0u - lv) & 0xFFFFu) * 0x00010001u;
                 uint32_t r[8];
@@ -316,7 +320,7 @@ __global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_
             const int X = (X0 >> 1) + qx, Y = (Y0 >> 1) + qy;
             if (X < a.W[1] && Y < a.H[1])
                 store_pairs(D1, a.dbytes[1], d_off32((X + Y) & 1, Y, X >> 1, a.H[1], a.Wc[1], Lp) + k * CH, acc);
-            if (a.F > 2) {
+            if (TXW == CP_T && a.F > 2) {
                 int4 *dst = reinterpret_cast<int4 *>(sD + (size_t)q * Lp + k * CH);
                 dst[0] = make_int4(acc[0] & 0xFFFF, acc[1] & 0xFFFF, acc[2] & 0xFFFF, acc[3] & 0xFFFF);
                 dst[1] = make_int4(acc[4] & 0xFFFF, acc[5] & 0xFFFF, acc[6] & 0xFFFF, acc[7] & 0xFFFF);
@@ -325,7 +329,7 @@ __global__ void __launch_bounds__(256, VSBP_CP_MINB) k_costpyr_fast(const uint8_
             }
         }
     }
-    upper_levels(a, sD, X0, Y0, b);
+    if (TXW == CP_T) upper_levels(a, sD, X0, Y0, b);
 }
 
 bool costpyr_fast_ok(const CostPyrArgs &a)
@@ -367,7 +371,25 @@ cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArg
         if (e != cudaSuccess) return e;
     }
     dim3 grid((a.W[0] + CP_T - 1) / CP_T, (a.H[0] + CP_T - 1) / CP_T, B);
-    if (costpyr_fast_ok(a) && a.L % CH == 0) {
+    static const bool wide = [] {
+        const char *e = getenv("VSBP_COSTPYR_WIDE");
+        return !(e && e[0] == '0');
+    }();
+    if (wide && a.F <= 2 && costpyr_fast_ok(a) && a.L % CH == 0 && a.nch == 4) {
+        // 16 x 32 tiles: levels 0-1 only (the deeper fused levels need 16 x 16 nesting)
+        constexpr int TXW = 2 * CP_T;
+        const size_t simg = ((size_t)CP_T * TXW + (size_t)CP_T * ((a.Lp + TXW - 9 + 3) & ~3) * 4 + 15) & ~(size_t)15;
+        static bool attr = false;
+        if (!attr && simg > 48 * 1024) {
+            cudaError_t e = cudaFuncSetAttribute(k_costpyr_fast<false, 4, TXW>,
+                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simg);
+            if (e != cudaSuccess) return e;
+            attr = true;
+        }
+        a.img_smem = (int)simg;
+        dim3 gw((a.W[0] + TXW - 1) / TXW, (a.H[0] + CP_T - 1) / CP_T, B);
+        k_costpyr_fast<false, 4, TXW><<<gw, 256, simg, st>>>(left, right, a);
+    } else if (costpyr_fast_ok(a) && a.L % CH == 0) {
         switch (a.nch) {
         case 1: k_costpyr_fast<false, 1><<<grid, 256, smem, st>>>(left, right, a); break;
         case 2: k_costpyr_fast<false, 2><<<grid, 256, smem, st>>>(left, right, a); break;
