@@ -371,24 +371,22 @@ cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArg
         if (e != cudaSuccess) return e;
     }
     dim3 grid((a.W[0] + CP_T - 1) / CP_T, (a.H[0] + CP_T - 1) / CP_T, B);
-    static const bool wide = [] {
+    // tile width (tuning knob VSBP_COSTPYR_WIDE: 16, 32 or 64 level-0 columns; default 64)
+    static const int wide = [] {
         const char *e = getenv("VSBP_COSTPYR_WIDE");
-        return !(e && e[0] == '0');
+        const int v = e ? atoi(e) : 64;  // measured 16 / 32 / 64: 7161 / 7198-7273 / 7326-7329 pairs/s
+        return v >= 64 ? 64 : (v >= 32 ? 32 : 16);
     }();
-    if (wide && a.F <= 2 && costpyr_fast_ok(a) && a.L % CH == 0 && a.nch == 4) {
-        // 16 x 32 tiles: levels 0-1 only (the deeper fused levels need 16 x 16 nesting)
-        constexpr int TXW = 2 * CP_T;
-        const size_t simg = ((size_t)CP_T * TXW + (size_t)CP_T * ((a.Lp + TXW - 9 + 3) & ~3) * 4 + 15) & ~(size_t)15;
-        static bool attr = false;
-        if (!attr && simg > 48 * 1024) {
-            cudaError_t e = cudaFuncSetAttribute(k_costpyr_fast<false, 4, TXW>,
-                                                 cudaFuncAttributeMaxDynamicSharedMemorySize, (int)simg);
-            if (e != cudaSuccess) return e;
-            attr = true;
-        }
+    if (wide > CP_T && a.F <= 2 && costpyr_fast_ok(a) && a.L % CH == 0 && a.nch == 4) {
+        // 16 x wide tiles: levels 0-1 only (the deeper fused levels need 16 x 16 nesting)
+        const size_t simg = ((size_t)CP_T * wide + (size_t)CP_T * ((a.Lp + wide - 9 + 3) & ~3) * 4 + 15) & ~(size_t)15;
+        if (a.Lp + wide > 256) return cudaErrorInvalidValue;  // staged window: <= 64 words per row
         a.img_smem = (int)simg;
-        dim3 gw((a.W[0] + TXW - 1) / TXW, (a.H[0] + CP_T - 1) / CP_T, B);
-        k_costpyr_fast<false, 4, TXW><<<gw, 256, simg, st>>>(left, right, a);
+        dim3 gw((a.W[0] + wide - 1) / wide, (a.H[0] + CP_T - 1) / CP_T, B);
+        if (wide == 64)
+            k_costpyr_fast<false, 4, 64><<<gw, 256, simg, st>>>(left, right, a);
+        else
+            k_costpyr_fast<false, 4, 32><<<gw, 256, simg, st>>>(left, right, a);
     } else if (costpyr_fast_ok(a) && a.L % CH == 0) {
         switch (a.nch) {
         case 1: k_costpyr_fast<false, 1><<<grid, 256, smem, st>>>(left, right, a); break;
