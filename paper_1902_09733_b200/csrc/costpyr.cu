@@ -371,11 +371,11 @@ cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArg
         if (e != cudaSuccess) return e;
     }
     dim3 grid((a.W[0] + CP_T - 1) / CP_T, (a.H[0] + CP_T - 1) / CP_T, B);
-    // tile width (tuning knob VSBP_COSTPYR_WIDE: 16, 32 or 64 level-0 columns; default 64)
+    // tile width (tuning knob VSBP_COSTPYR_WIDE: 16, 32, 64 or 128 level-0 columns; default 128)
     static const int wide = [] {
         const char *e = getenv("VSBP_COSTPYR_WIDE");
-        const int v = e ? atoi(e) : 64;  // measured 16 / 32 / 64: 7161 / 7198-7273 / 7326-7329 pairs/s
-        return v >= 64 ? 64 : (v >= 32 ? 32 : 16);
+        const int v = e ? atoi(e) : 128;  // measured 16 / 32 / 64 / 128: 7161 / 7198-7273 / 7302-7349 / 7361 pairs/s
+        return v >= 128 ? 128 : (v >= 64 ? 64 : (v >= 32 ? 32 : 16));
     }();
     if (wide > CP_T && a.F <= 2 && costpyr_fast_ok(a) && a.L % CH == 0 && a.nch == 4) {
         // 16 x wide tiles: levels 0-1 only (the deeper fused levels need 16 x 16 nesting)
@@ -383,7 +383,9 @@ cudaError_t launch_costpyr(const uint8_t *left, const uint8_t *right, CostPyrArg
         if (a.Lp + wide > 256) return cudaErrorInvalidValue;  // staged window: <= 64 words per row
         a.img_smem = (int)simg;
         dim3 gw((a.W[0] + wide - 1) / wide, (a.H[0] + CP_T - 1) / CP_T, B);
-        if (wide == 64)
+        if (wide == 128)
+            k_costpyr_fast<false, 4, 128><<<gw, 256, simg, st>>>(left, right, a);
+        else if (wide == 64)
             k_costpyr_fast<false, 4, 64><<<gw, 256, simg, st>>>(left, right, a);
         else
             k_costpyr_fast<false, 4, 32><<<gw, 256, simg, st>>>(left, right, a);
