@@ -247,7 +247,10 @@ template <> struct GuideVec<2> {  // 6 bytes, 2-byte aligned
 };
 
 template <int R, int S, int NR, int P>
-__global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? 5 : 8) : (P == 4 ? 3 : 4)) k_jbu_vec(const int32_t *__restrict__ disp_lo,
+#ifndef VSBP_JBU_MINB
+#define VSBP_JBU_MINB 5  // resident CTAs per SM for the 2-row, 4-pixel variant (the bench's s = 4)
+#endif
+__global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU_MINB : 8) : (P == 4 ? 3 : 4)) k_jbu_vec(const int32_t *__restrict__ disp_lo,
                                                            const uint8_t *__restrict__ guide,
                                                            float *__restrict__ disp_hi, float *__restrict__ xyz,
                                                            unsigned long long *__restrict__ n_valid,
