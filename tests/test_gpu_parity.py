@@ -149,6 +149,15 @@ def test_generic_and_fused_kernels_agree_with_oracle(W, H, L, levels):
                 Dl = oracle.pyramid_down(Dl)
 
 
+@pytest.mark.parametrize("W,H,L", [(127, 19, 64), (129, 17, 49), (256, 33, 57), (301, 37, 64), (385, 18, 60)])
+def test_costpyr_wide_tiles_ragged(W, H, L):
+    """The 16 x 128 cost-volume tiles (levels 0-1 fused, Lp = 64): widths one
+    column short of, just past and several tiles beyond 128 columns, odd heights,
+    L below Lp; costs and messages on every level vs the oracle."""
+    l, r, _ = synthgen.row_plane_pair(7 + W, W, H, 1, 40)
+    check_bp_case(l, r, L, 4, 2)
+
+
 def test_batch_equals_single():
     pairs = [synthgen.shifted_pair(10 + i, 80, 50, 3 + i) for i in range(3)]
     left = np.stack([p[0] for p in pairs])
