@@ -38,6 +38,11 @@
 
 namespace vsbp {
 
+// JB_RP: row passes per CTA of the vector kernel (one staged footprint serves
+// JB_RP x JB_Y rows; fewer redundantly staged halo rows per pixel)
+#ifndef JB_RP
+#define JB_RP 2
+#endif
 constexpr int JB_X = 32, JB_Y = 8, JB_RMAX = 8, JB_SMAX = 16, JB_TMAX = 2 * JB_RMAX + 1;
 constexpr int JB_LW = JB_X + 2 * JB_RMAX + 1, JB_LH = JB_Y + 2 * JB_RMAX + 1;
 
@@ -264,14 +269,18 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     __shared__ unsigned warp_cnt[NT / 32];
     const int b = blockIdx.z;
     const int Wh = a.W * S, Hh = a.H * S;
-    const int x0 = blockIdx.x * (JB_X * P), y0 = blockIdx.y * JB_Y;
+    const int x0 = blockIdx.x * (JB_X * P), y0 = blockIdx.y * (JB_Y * JB_RP);
     const int lx0 = x0 / S - R, ly0 = y0 / S - R;
     const int lw = min(x0 + JB_X * P - 1, Wh - 1) / S + R - lx0 + 1;
-    const int lh = min(y0 + JB_Y - 1, Hh - 1) / S + R - ly0 + 1;
+    const int lh = min(y0 + JB_Y * JB_RP - 1, Hh - 1) / S + R - ly0 + 1;
     const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
     stage_taps(sT, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, S, Wh, a, NT);
     __syncthreads();
-    const int x = x0 + P * threadIdx.x, yb = y0 + NR * threadIdx.y;
+    const int x = x0 + P * threadIdx.x;
+    int cnt = 0;
+#pragma unroll 1
+    for (int rp = 0; rp < JB_RP; ++rp) {
+    const int yb = y0 + rp * JB_Y + NR * threadIdx.y;
     const bool inside = x < Wh && yb < Hh;  // Wh % P == 0, Hh % NR == 0: all pixels or none
     float Dp[NR][P];
 #pragma unroll
@@ -395,9 +404,9 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
                 *reinterpret_cast<float2 *>(dst) = make_float2(Dp[r][0], Dp[r][1]);
         }
     }
-    if (!a.do_xyz) return;
+    if (!a.do_xyz) continue;
     // ---- a7: 3P contiguous floats per thread and row, pixel pairs on FFMA2
-    int cnt = 0;
+
     f2_t q2[16];
 #pragma unroll
     for (int i = 0; i < 16; ++i) q2[i] = pk2(a.q[i], a.q[i]);
@@ -442,7 +451,8 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
             }
         }
     }
-    block_count(warp_cnt, cnt, n_valid, b, NT / 32);
+    }
+    if (a.do_xyz) block_count(warp_cnt, cnt, n_valid, b, NT / 32);
 }
 
 // ---------------------------------------------------------------- launch
@@ -500,7 +510,7 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     const bool vec = (s == 2 || s == 4 || s == 8) && radius <= JB_RVEC && al(guide, P == 4 ? 4 : 2) &&
                      al(disp_hi, 4 * P) && al(xyz, 4 * P);
     if (vec) {
-        dim3 grid((W * s + JB_X * P - 1) / (JB_X * P), (H * s + JB_Y - 1) / JB_Y, B);
+        dim3 grid((W * s + JB_X * P - 1) / (JB_X * P), (H * s + JB_Y * JB_RP - 1) / (JB_Y * JB_RP), B);
         if (s == 2)
             launch_vec<2, 2>(radius, grid, st, disp_lo, guide, disp_hi, xyz, n_valid, a);
         else if (s == 4)
