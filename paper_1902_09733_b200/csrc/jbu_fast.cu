@@ -74,8 +74,17 @@ __device__ __forceinline__ void stage_taps(uint2 *sT, const uint8_t *G, const in
                                            int lh, int s, int Wh, const JbuFastArgs &a, int nthreads)
 {
     const int tid = threadIdx.y * JB_X + threadIdx.x;
+    // (ey, ex) = (e / lw, e % lw) advanced incrementally: two divides per thread
+    const int sy = nthreads / lw, sx = nthreads - sy * lw;
+    int ey = tid / lw, ex = tid - ey * lw;
     for (int e = tid; e < lw * lh; e += nthreads) {
-        const int qy = min(max(ly0 + e / lw, 0), a.H - 1), qx = min(max(lx0 + e % lw, 0), a.W - 1);
+        const int qy = min(max(ly0 + ey, 0), a.H - 1), qx = min(max(lx0 + ex, 0), a.W - 1);
+        ey += sy;
+        ex += sx;
+        if (ex >= lw) {
+            ex -= lw;
+            ++ey;
+        }
         const uint8_t *g = G + ((size_t)(s * qy + s / 2) * Wh + (size_t)(s * qx + s / 2)) * 3;
         uint2 rec;
         rec.x = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
