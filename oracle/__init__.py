@@ -22,6 +22,9 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 _SRC = os.path.join(_HERE, "vsbp_oracle.c")
 _LIB = os.path.join(_HERE, "liboracle.so")
+# VSBP_ORACLE_LIB: load a deliberately MUTATED build of vsbp_oracle.c instead
+# (tools/mutation_check.py: proves each pin fails under a plausible mistake)
+_LIB_OVERRIDE = os.environ.get("VSBP_ORACLE_LIB")
 
 _ERR = {0: "ok", -1: "EINVAL", -2: "EDIM", -3: "EOVERFLOW"}
 
@@ -34,6 +37,8 @@ class OracleError(RuntimeError):
 
 def build(force: bool = False) -> str:
     """Compile the oracle with plain gcc -O2 (no SIMD flags, no fast-math)."""
+    if _LIB_OVERRIDE:
+        return _LIB_OVERRIDE
     if force or not os.path.exists(_LIB) or os.path.getmtime(_LIB) < os.path.getmtime(_SRC):
         tmp = _LIB + f".tmp{os.getpid()}"
         subprocess.check_call(["gcc", "-O2", "-std=c11", "-shared", "-fPIC", "-o", tmp, _SRC, "-lm"])
@@ -47,8 +52,8 @@ _lib = None
 def lib():
     global _lib
     if _lib is None:
-        build()
-        L = C.CDLL(_LIB)
+        path = build()
+        L = C.CDLL(path)
         p = C.c_void_p
         i = C.c_int
         f = C.c_float
@@ -59,6 +64,7 @@ def lib():
         L.oracle_remap_rgb.argtypes = [p, i, i, p, p, p]
         L.oracle_harris_response.argtypes = [p, i, i, p]
         L.oracle_csbp.argtypes = [p, p, i, i, i, i, i, i, f, f, f, p, p]
+        L.oracle_csbp_costs.argtypes = [p, i, i, i, i, i, i, C.c_int32, C.c_int32, p, p, p]
         L.oracle_harris_grid.argtypes = [p, i, i, i, i, i, C.c_int64, p, p, p]
         L.oracle_zssd.argtypes = [p, p, i, i, i, i, i, i, i, p]
         L.oracle_zssd_match.argtypes = [p, p, i, i, p, i, i, i, C.c_int64, p, p]
@@ -183,6 +189,28 @@ def csbp_disparity(left, right, L, levels, iters, k0, lam=0.07, data_trunc=15.0,
         out.append(cand[off:off + w * h * k].reshape(h, w, k))
         off += w * h * k
     return disp, out
+
+
+def csbp_costs(D0: np.ndarray, levels: int, iters: int, k0: int, S: int, tau_q: int):
+    """f2 on a given level-0 data term D0 int32 [H][W][L] (R-32..R-35 with the
+    smoothness (S, tau_q) given directly).  Returns (disp [H][W], candidates per
+    level [H_l][W_l][k_l], final incoming messages per level [H_l][W_l][4][k_l])."""
+    D0 = np.ascontiguousarray(D0, np.int32)
+    H, W, L = D0.shape
+    disp = np.zeros((H, W), np.int32)
+    dims = level_dims(W, H, levels)
+    ks = csbp_k(L, levels, k0)
+    cand = np.zeros(sum(w * h * k for (w, h), k in zip(dims, ks)), np.int32)
+    msg = np.zeros(sum(w * h * 4 * k for (w, h), k in zip(dims, ks)), np.int32)
+    _check(lib().oracle_csbp_costs(_ptr(D0), W, H, L, levels, iters, k0, S, tau_q, _ptr(disp), _ptr(cand),
+                                   _ptr(msg)), "oracle_csbp_costs")
+    cands, msgs, oc, om = [], [], 0, 0
+    for (w, h), k in zip(dims, ks):
+        cands.append(cand[oc:oc + w * h * k].reshape(h, w, k))
+        msgs.append(msg[om:om + w * h * 4 * k].reshape(h, w, 4, k))
+        oc += w * h * k
+        om += w * h * 4 * k
+    return disp, cands, msgs
 
 
 def harris_response(img: np.ndarray) -> np.ndarray:

@@ -812,18 +812,27 @@ static void select_k(const int64_t *score, const int32_t *key, int n, int k, int
     free(sel);
 }
 
-int oracle_csbp(const uint8_t *left, const uint8_t *right, int W, int H, int L, int levels, int iters, int k0,
-                float lambda, float data_trunc, float disc_trunc, int32_t *disp, int32_t *cand_out)
+/* CSBP on a given level-0 data term D0 (i32 [H][W][L], any values >= 0), the
+ * quantised smoothness (S, tau_q) given directly.  msg_out (optional): every
+ * level's final incoming messages, level 0 first, each [H_l][W_l][4][k_l]
+ * (in[p][k][i] as defined above).  Domain: max(D0) * 4^(levels-1) + 4 tau_q +
+ * 2^20 < 2^31 (the R-25 bound with max D0 in place of lambda_q tau_d). */
+int oracle_csbp_costs(const int32_t *D0, int W, int H, int L, int levels, int iters, int k0, int32_t S,
+                      int32_t tau_q, int32_t *disp, int32_t *cand_out, int32_t *msg_out)
 {
-    if (!left || !right || !disp || W < 1 || H < 1 || L < 2 || levels < 1 || levels > 16 || iters < 1 || k0 < 1)
+    if (!D0 || !disp || W < 1 || H < 1 || L < 2 || levels < 1 || levels > 16 || iters < 1 || k0 < 1 || S < 0 ||
+        tau_q < 0)
         return OR_EINVAL;
-    int32_t q[4];
-    int rc = oracle_quantize(lambda, data_trunc, disc_trunc, q);
-    if (rc) return rc;
-    int32_t lam_q = q[0], tau_d = q[1], tau_q = q[2], S = q[3];
-    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q +
-                    ((int64_t)1 << 20);
-    if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
+    {
+        int64_t dmax = 0;
+        for (size_t i = 0; i < (size_t)W * H * L; ++i) {
+            if (D0[i] < 0) return OR_EINVAL;
+            if (D0[i] > dmax) dmax = D0[i];
+        }
+        int64_t bound = dmax * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q + ((int64_t)1 << 20);
+        if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
+    }
+    int rc;
     int Ws[16], Hs[16], K[16];
     level_dims(W, H, levels, Ws, Hs);
     for (int l = 0; l < levels; ++l) {
@@ -839,8 +848,7 @@ int oracle_csbp(const uint8_t *left, const uint8_t *right, int W, int H, int L, 
         M[l] = (int32_t *)calloc(n * 4 * K[l], sizeof(int32_t));
         if (!Dl[l] || !C[l] || !M[l]) { rc = OR_EINVAL; goto done; }
     }
-    rc = oracle_cost_volume(left, right, W, H, L, lam_q, tau_d, Dl[0]);
-    if (rc) goto done;
+    memcpy(Dl[0], D0, sizeof(int32_t) * (size_t)W * H * L);
     for (int l = 0; l + 1 < levels; ++l) {
         rc = oracle_pyramid_down(Dl[l], Ws[l], Hs[l], L, Dl[l + 1]);
         if (rc) goto done;
@@ -962,7 +970,36 @@ int oracle_csbp(const uint8_t *left, const uint8_t *right, int W, int H, int L, 
             off += n;
         }
     }
+    if (msg_out) {
+        size_t off = 0;
+        for (int l = 0; l < levels; ++l) {
+            size_t n = (size_t)Ws[l] * Hs[l] * 4 * K[l];
+            memcpy(msg_out + off, M[l], sizeof(int32_t) * n);
+            off += n;
+        }
+    }
 done:
     for (int l = 0; l < levels; ++l) { free(Dl[l]); free(C[l]); free(M[l]); }
+    return rc;
+}
+
+/* CSBP from the image pair: D0 = the cost volume of O2, then oracle_csbp_costs. */
+int oracle_csbp(const uint8_t *left, const uint8_t *right, int W, int H, int L, int levels, int iters, int k0,
+                float lambda, float data_trunc, float disc_trunc, int32_t *disp, int32_t *cand_out)
+{
+    if (!left || !right || !disp || W < 1 || H < 1 || L < 2 || levels < 1 || levels > 16 || iters < 1 || k0 < 1)
+        return OR_EINVAL;
+    int32_t q[4];
+    int rc = oracle_quantize(lambda, data_trunc, disc_trunc, q);
+    if (rc) return rc;
+    int32_t lam_q = q[0], tau_d = q[1], tau_q = q[2], S = q[3];
+    int64_t bound = (int64_t)lam_q * tau_d * ((int64_t)1 << (2 * (levels - 1))) + 4 * (int64_t)tau_q +
+                    ((int64_t)1 << 20);
+    if (bound >= ((int64_t)1 << 31)) return OR_EOVERFLOW;
+    int32_t *D0 = (int32_t *)malloc(sizeof(int32_t) * (size_t)W * H * L);
+    if (!D0) return OR_EINVAL;
+    rc = oracle_cost_volume(left, right, W, H, L, lam_q, tau_d, D0);
+    if (!rc) rc = oracle_csbp_costs(D0, W, H, L, levels, iters, k0, S, tau_q, disp, cand_out, NULL);
+    free(D0);
     return rc;
 }

@@ -10,8 +10,9 @@ import pytest
 
 import oracle
 import synthgen
-from brute import (beliefs, brute_message, chain_min_marginals, energy, exhaustive_map,
-                   jacobi_bp, jbu_literal, project)
+from brute import (OPP, DIRS, beliefs, brute_message, chain_min_marginals, checkerboard_via_jacobi,
+                   constant_space_bp, csbp_select, energy, exhaustive_map, hierarchical_bp, jacobi_bp,
+                   jbu_literal, np_cost_volume, np_pyramid, project)
 
 Q0 = oracle.quantize(0.07, 15.0, 1.7)
 
@@ -185,6 +186,132 @@ def test_hierarchical_chain_forgets_init(seed):
     mu = chain_min_marginals(D[0], Q0.S, Q0.tau_q)
     assert np.array_equal(b - b.min(axis=1, keepdims=True), mu - mu.min(axis=1, keepdims=True))
     assert np.array_equal(disp[0], np.argmin(mu, axis=1))
+
+
+HIER_PARAMS = [(0.07, 15.0, 1.7), (0.3, 40.0, 0.6), (1.0, 8.0, 3.0), (0.07, 15.0, 0.2)]
+
+
+@pytest.mark.parametrize("seed", range(30))
+def test_hierarchy_equals_jacobi_from_upcopy(seed):
+    """P:30 [4], R-10, R-12: the whole coarse-to-fine wiring against an independent
+    construction (tests/brute.py hierarchical_bp): numpy cost volume and ceil 2x2
+    pyramid, np.repeat up-copy with the edge mask, and every level's checkerboard
+    state rebuilt from synchronous BP started at the up-copied messages with t
+    restarting at 0 on each level.  Loopy grids with few iterations do NOT forget
+    their initialisation, so a wrong parent index, edge mask or colour order on any
+    level changes the level-0 messages.  Every level's messages and the disparity
+    must agree exactly."""
+    rng = np.random.default_rng(500 + seed)
+    W, H = int(rng.integers(2, 9)), int(rng.integers(2, 8))
+    L = int(rng.integers(2, 6))
+    levels = int(rng.integers(2, 5))
+    iters = int(rng.integers(1, 7))
+    lam, dt, st = HIER_PARAMS[seed % len(HIER_PARAMS)]
+    left = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    right = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    q = oracle.quantize(lam, dt, st)
+    disp, msgs = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
+    disp_b, msgs_b = hierarchical_bp(left, right, L, levels, iters, q)
+    for lv in range(levels):
+        assert np.array_equal(msgs[lv], msgs_b[lv]), (seed, lv)
+    assert np.array_equal(disp, disp_b)
+
+
+def _k_cheap_costs(rng, H, W, L, k, tau_q):
+    """Level-0 data term where every pixel has exactly k 'cheap' labels (random
+    subset, costs in [0, 600)) and the rest cost more than 600 + 4 tau_q: no
+    belief of an expensive label can win, and no expensive sender label can reach
+    a message's minimum (h >= min h + tau_q there)."""
+    D = rng.integers(0, 600, size=(H, W, L)).astype(np.int64)
+    for y in range(H):
+        for x in range(W):
+            exp = rng.permutation(L)[k:]
+            D[y, x, exp] = 600 + 4 * tau_q + 1 + rng.integers(0, 500, size=exp.size)
+    return D.astype(np.int32)
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_csbp_k_below_L_equals_full_bp(seed):
+    """R-35 with k < L and different candidate sets at neighbouring pixels: when
+    exactly k labels per pixel are cheap (the rest dominated, see _k_cheap_costs),
+    one-level CSBP keeps exactly those, and its messages are the full BP's messages
+    (synchronous brute BP, not the oracle) restricted to the RECEIVER's candidates
+    minus their minimum; the disparities are equal.  A message that measured
+    |c_p[i] - c_p[j]| instead of |c_p[i] - c_q[j]| breaks this."""
+    rng = np.random.default_rng(600 + seed)
+    W, H = int(rng.integers(2, 9)), int(rng.integers(1, 7))
+    L = int(rng.integers(4, 11))
+    k = int(rng.integers(2, L))
+    iters = int(rng.integers(1, 8))
+    S, tau = int(rng.choice([16, 128])), int(rng.integers(40, 420))
+    D = _k_cheap_costs(rng, H, W, L, k, tau)
+    disp, cands, msgs = oracle.csbp_costs(D, 1, iters, k, S, tau)
+    cheap = np.sort(np.argsort(D, axis=2, kind="stable")[:, :, :k], axis=2)
+    assert np.array_equal(cands[0], cheap)
+    M = checkerboard_via_jacobi(D, S, tau, iters, np.zeros((4, H, W, L), np.int64))
+    for y in range(H):
+        for x in range(W):
+            c = cands[0][y, x]
+            for kk, (dx, dy) in enumerate(DIRS):
+                qx, qy = x + dx, y + dy
+                got = msgs[0][y, x, kk]
+                if not (0 <= qx < W and 0 <= qy < H):
+                    assert not got.any()
+                    continue
+                ref = M[OPP[kk], qy, qx][c]
+                assert np.array_equal(got, ref - ref.min()), (seed, x, y, kk)
+    assert np.array_equal(disp, np.argmin(beliefs(D, M), axis=2))
+
+
+@pytest.mark.parametrize("seed", range(24))
+def test_csbp_hierarchy_equals_brute(seed):
+    """R-32..R-35 across levels against tests/brute.py constant_space_bp (numpy
+    pyramid, lexsort selection by D + the parent's final incoming messages,
+    receiver-side inheritance with the edge mask, synchronous O(k^2) messages with
+    the truncation inside V, checkerboard state rebuilt from Jacobi steps):
+    candidates, final messages and disparities of every level agree exactly."""
+    rng = np.random.default_rng(700 + seed)
+    W, H = int(rng.integers(2, 9)), int(rng.integers(2, 8))
+    L = int(rng.integers(4, 10))
+    levels = int(rng.integers(2, 4))
+    k0 = int(rng.integers(1, 4))
+    iters = int(rng.integers(1, 6))
+    S, tau = int(rng.choice([16, 128])), int(rng.integers(40, 420))
+    if seed % 2:
+        D = rng.integers(0, 900, size=(H, W, L)).astype(np.int32)
+    else:
+        left = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        right = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+        D = np_cost_volume(left, right, L, 9, 15).astype(np.int32)
+    disp, cands, msgs = oracle.csbp_costs(D, levels, iters, k0, S, tau)
+    disp_b, cands_b, msgs_b = constant_space_bp(D, levels, iters, k0, S, tau)
+    for lv in range(levels):
+        assert np.array_equal(cands[lv], cands_b[lv]), (seed, lv)
+        assert np.array_equal(msgs[lv], msgs_b[lv]), (seed, lv)
+    assert np.array_equal(disp, disp_b)
+
+
+def test_csbp_selection_is_least_score_at_every_level():
+    """R-34 step by step on a larger grid: level l's candidates are the k_l labels
+    of the parent's pool with least D_l(p, d) + sum_k in_parent[k](d) (the parent's
+    FINAL incoming messages), ties to the smaller label -- by np.lexsort."""
+    rng = np.random.default_rng(11)
+    H, W, L, levels, k0 = 19, 26, 20, 3, 2
+    D = rng.integers(0, 2000, size=(H, W, L)).astype(np.int32)
+    _, cands, msgs = oracle.csbp_costs(D, levels, 3, k0, 128, 218)
+    Ds = [D.astype(np.int64)]
+    for _ in range(levels - 1):
+        Ds.append(np_pyramid(Ds[-1]))
+    n_msg_decided = 0
+    for lv in range(levels - 1):
+        for y in range(Ds[lv].shape[0]):
+            for x in range(Ds[lv].shape[1]):
+                pool = cands[lv + 1][y // 2, x // 2]
+                score = Ds[lv][y, x, pool] + msgs[lv + 1][y // 2, x // 2].sum(axis=0)
+                sel = csbp_select(score, pool, cands[lv].shape[2])
+                assert np.array_equal(cands[lv][y, x], pool[sel]), (lv, x, y)
+                n_msg_decided += not np.array_equal(np.sort(csbp_select(Ds[lv][y, x, pool], pool, sel.size)), sel)
+    assert n_msg_decided > 50  # the messages change the selection at many pixels
 
 
 def test_upcopy_hand_and_constant():
@@ -691,3 +818,17 @@ def test_icp_nearest_is_brute_force_minimum():
     j, d2 = icp.nearest(P, Q, chunk=5)
     full = ((P[:, None, :] - Q[None, :, :]) ** 2).sum(axis=2)
     assert np.array_equal(j, full.argmin(axis=1)) and np.allclose(d2, full.min(axis=1), rtol=1e-15)
+
+
+# ----------------------------------------------------------------------------- the pins bite
+def test_oracle_mutations_are_caught():
+    """tools/mutation_check.py: every plausible mistake listed there (t carried
+    across levels, wrong parent index, cp[j] for cq[j], pool scored by D only, ...)
+    makes at least one pin above fail; documented equivalent mutants excepted."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, os.path.join(root, "tools", "mutation_check.py"), "--fast"],
+                       capture_output=True, text=True, timeout=900)
+    assert r.returncode == 0, r.stdout + r.stderr
