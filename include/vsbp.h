@@ -142,7 +142,12 @@ void bp_destroy(vsbp_bp *ctx);
  *               window's weights would leave f32 range); sigma_r: range sigma on
  *               the 0..255 scale (> 0); radius: window half-width in low-res
  *               pixels, 1..8; s: integer scale 1..16.
- * f32 arithmetic; agrees with the double oracle within 1e-4 full-res px.
+ * Accuracy: agrees with the double oracle within 1e-4 full-res px for every
+ * output below 2048 px, and within one f32 ulp of it above (the float output
+ * cannot be closer there), for any int32 labels |D'| < 2^24.  Windows whose
+ * label spread times s is at most 256 run in f32 on residual labels
+ * (D'_q - D'_centre; error ~2e-7 * s * spread); wider windows are computed with
+ * double weights and sums (slower, rare on smooth maps).
  * jbu_upsample is the B = 1 case.
  * ------------------------------------------------------------------------- */
 int jbu_upsample_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s,

@@ -2,7 +2,8 @@
 // reprojection (a7, Eq.3) and the valid-point count, sm_100a.
 //
 // Eq.2 with R-15..R-19, R-24: for full-res pixel p, taps q in the (2R+1)^2 window
-// around c = floor(p/s):  D_p = s * sum_q w_q D'_q / sum_q w_q,
+// around c = floor(p/s):  D_p = s * sum_q w_q D'_q / sum_q w_q
+//                              = s * (D'_c + sum_q w_q (D'_q - D'_c) / sum_q w_q),
 //   log2 w_q = sx[tx] + sy[ty] - cr * (dist2(I_p, I_q) - ref)
 // with sx, sy = -log2(e)|p_down - q|^2/(2 sigma_s^2) split per axis (separable),
 // cr = log2(e)/(2 sigma_r^2), dist2 = the exact integer squared RGB distance
@@ -14,6 +15,17 @@
 // is tiny), else the window minimum (an extra integer pass).  Out-of-image taps
 // get sx = -inf or a row factor of 0 (weight 0): "taps outside the low-res image
 // are skipped".  Rows are accumulated separately and scaled by 2^sy at the end.
+//
+// Accuracy (include/vsbp.h jbu_upsample_batch): the sums accumulate the RESIDUAL
+// labels D'_q - D'_c (D'_c = the window centre's label), so the f32 error is
+// relative to the label spread of the window, not to the output's magnitude:
+// |err| ~ 2e-7 * s * spread full-res px (ex2.approx and rcp.approx are ~2^-22).  A
+// window with s * spread > spread_max (256: error <= ~5e-5 px) is computed on the
+// PRECISE path instead -- double weights (exp2 in f64) and double sums, one pixel
+// at a time (jbu_precise_px).  The test is CTA-uniform first (the staged tile's
+// label range, a free by-product of the staging) and per window only inside wide
+// tiles, so smooth maps never pay for it.  Both kernels take the same decision per
+// window and run the same arithmetic: bit-identical outputs.
 //
 // Two kernels, the same arithmetic in the same order (bit-identical results):
 //  * k_jbu_vec<R,S> (s = S in {2,4,8}): a thread owns P = min(S,4) horizontally
@@ -29,6 +41,7 @@
 // sample + label) are staged once in shared memory as 8-byte records.  The reprojection
 // [X Y Z W] = Q [u v D_p 1] follows in registers (one reciprocal of W per pixel);
 // one atomic per block counts the points with D_p >= min_disp.
+#include <limits.h>
 #include <math.h>
 #include <stdlib.h>
 #include <string.h>
@@ -49,6 +62,8 @@ constexpr int JB_LW = JB_X + 2 * JB_RMAX + 1, JB_LH = JB_Y + 2 * JB_RMAX + 1;
 struct JbuFastArgs {
     int W, H, s;
     float cr;
+    float spread_max;             // s * (window label spread) above which the precise path runs
+    double cs2, cr2;              // log2(e)/(2 sigma_s^2), log2(e)/(2 sigma_r^2) for the precise path
     int far_thr;                  // centre dist2 above which the window minimum is the reference
     float sxt[JB_SMAX][JB_TMAX];  // [x mod s][tap column]: log2 of the x spatial weight
     float ryt[JB_SMAX][JB_TMAX];  // [y mod s][tap row]: the y spatial weight 2^sy
@@ -70,10 +85,13 @@ __device__ __forceinline__ float ex2(float x)
 // in-image tap (clamped coordinates), which lies in every window that contains the
 // phantom, so its colour distance is >= the window minimum and its exponent never
 // overflows (0 * inf would be NaN).
-__device__ __forceinline__ void stage_taps(uint2 *sT, const uint8_t *G, const int32_t *Dl, int lx0, int ly0, int lw,
-                                           int lh, int s, int Wh, const JbuFastArgs &a, int nthreads)
+// Each warp also leaves the min / max of the labels it staged in wlo / whi[warp]
+// (the tile's label range after the barrier, tile_range()).
+__device__ __forceinline__ void stage_taps(uint2 *sT, int *wlo, int *whi, const uint8_t *G, const int32_t *Dl, int lx0,
+                                           int ly0, int lw, int lh, int s, int Wh, const JbuFastArgs &a, int nthreads)
 {
     const int tid = threadIdx.y * JB_X + threadIdx.x;
+    int lo = INT_MAX, hi = INT_MIN;
     // (ey, ex) = (e / lw, e % lw) advanced incrementally: two divides per thread
     const int sy = nthreads / lw, sx = nthreads - sy * lw;
     int ey = tid / lw, ex = tid - ey * lw;
@@ -88,9 +106,90 @@ __device__ __forceinline__ void stage_taps(uint2 *sT, const uint8_t *G, const in
         const uint8_t *g = G + ((size_t)(s * qy + s / 2) * Wh + (size_t)(s * qx + s / 2)) * 3;
         uint2 rec;
         rec.x = (unsigned)g[0] | ((unsigned)g[1] << 8) | ((unsigned)g[2] << 16);
-        rec.y = __float_as_uint((float)Dl[(size_t)qy * a.W + qx]);
+        const int lab = Dl[(size_t)qy * a.W + qx];
+        lo = min(lo, lab);
+        hi = max(hi, lab);
+        rec.y = __float_as_uint((float)lab);
         sT[e] = rec;
     }
+    lo = __reduce_min_sync(FULL, lo);
+    hi = __reduce_max_sync(FULL, hi);
+    if ((threadIdx.x & 31) == 0) {
+        wlo[tid >> 5] = lo;
+        whi[tid >> 5] = hi;
+    }
+}
+
+// after the staging barrier: is s * (tile label range) above spread_max?  (CTA-uniform)
+__device__ __forceinline__ bool tile_wide(const int *wlo, const int *whi, int nwarps, const JbuFastArgs &a)
+{
+    int lo = wlo[0], hi = whi[0];
+    for (int w = 1; w < nwarps; ++w) {
+        lo = min(lo, wlo[w]);
+        hi = max(hi, whi[w]);
+    }
+    return (float)a.s * (float)((long long)hi - lo) > a.spread_max;
+}
+
+// the window of (cx, cy) needs the precise path: s * (max - min label over its
+// in-image taps) > spread_max (win = the staged window's first record)
+template <int R>
+__device__ __forceinline__ bool window_wide(const uint2 *win, int lw, int cx, int cy, const JbuFastArgs &a)
+{
+    float lo = __uint_as_float(win[R * lw + R].y), hi = lo;
+#pragma unroll 1
+    for (int ty = 0; ty <= 2 * R; ++ty) {
+        const int qy = cy - R + ty;
+        if (qy < 0 || qy >= a.H) continue;
+#pragma unroll 1
+        for (int tx = 0; tx <= 2 * R; ++tx) {
+            const int qx = cx - R + tx;
+            if (qx < 0 || qx >= a.W) continue;
+            const float v = __uint_as_float(win[ty * lw + tx].y);
+            lo = fminf(lo, v);
+            hi = fmaxf(hi, v);
+        }
+    }
+    return (float)a.s * (hi - lo) > a.spread_max;
+}
+
+// The precise path for one pixel (sub-position u, v of its footprint; colour Ip):
+// Eq.2 with double weights w_q = 2^(logit_q - max logit) over the in-image taps
+// and double sums of w_q (D'_q - D'_c); the result rounded once to f32.
+template <int R>
+__device__ __noinline__ float jbu_precise_px(const uint2 *win, int lw, unsigned Ip, int u, int v, int cx, int cy,
+                                             const JbuFastArgs &a)
+{
+    const double fx = ((double)u + 0.5) / a.s - 0.5 + R, fy = ((double)v + 0.5) / a.s - 0.5 + R;
+    const double c = (double)__uint_as_float(win[R * lw + R].y);
+    double lmax = -INFINITY;
+#pragma unroll 1
+    for (int pass = 0; pass < 2; ++pass) {
+        double num = 0.0, den = 0.0;
+#pragma unroll 1
+        for (int ty = 0; ty <= 2 * R; ++ty) {
+            const int qy = cy - R + ty;
+            if (qy < 0 || qy >= a.H) continue;
+#pragma unroll 1
+            for (int tx = 0; tx <= 2 * R; ++tx) {
+                const int qx = cx - R + tx;
+                if (qx < 0 || qx >= a.W) continue;
+                const uint2 t = win[ty * lw + tx];
+                const unsigned ad = __vabsdiffu4(Ip, t.x);
+                const double sx = fx - tx, sy = fy - ty;
+                const double logit = -a.cs2 * (sx * sx + sy * sy) - a.cr2 * (double)__dp4a(ad, ad, 0u);
+                if (pass == 0) {
+                    lmax = fmax(lmax, logit);
+                } else {
+                    const double w = exp2(logit - lmax);
+                    num = fma(w, (double)__uint_as_float(t.y) - c, num);
+                    den += w;
+                }
+            }
+        }
+        if (pass == 1) return (float)((double)a.s * (c + num / den));
+    }
+    return 0.f;  // not reached
 }
 
 // n / d with one MUFU.RCP (rel. error ~2^-22; the tolerances are 1e-4 px / 1e-5 rel)
@@ -141,6 +240,7 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
     constexpr int T = 2 * R + 1;
     __shared__ uint2 sT[JB_LW * JB_LH];
     __shared__ unsigned warp_cnt[JB_Y];
+    __shared__ int wlo[JB_Y], whi[JB_Y];
     const int b = blockIdx.z;
     const int s = a.s;
     const int Wh = a.W * s, Hh = a.H * s;
@@ -149,8 +249,9 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
     const int lw = min(x0 + JB_X - 1, Wh - 1) / s + R - lx0 + 1;
     const int lh = min(y0 + JB_Y - 1, Hh - 1) / s + R - ly0 + 1;
     const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
-    stage_taps(sT, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, s, Wh, a, JB_X * JB_Y);
+    stage_taps(sT, wlo, whi, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, s, Wh, a, JB_X * JB_Y);
     __syncthreads();
+    const bool wide = tile_wide(wlo, whi, JB_Y, a);
     const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
     const bool inside = x < Wh && y < Hh;
     float Dp = 0.f;
@@ -167,6 +268,10 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
             rfl[t] = (qy >= 0 && qy < a.H) ? a.ryt[v][t] : 0.f;
         }
         const int e0 = (cy - R - ly0) * lw + (cx - R - lx0);
+        const float cf = __uint_as_float(sT[e0 + R * lw + R].y);
+        if (wide && window_wide<R>(sT + e0, lw, cx, cy, a)) {
+            Dp = jbu_precise_px<R>(sT + e0, lw, Ip, u, v, cx, cy, a);
+        } else {
         const unsigned ad = __vabsdiffu4(Ip, sT[e0 + R * lw + R].x);
         int ref = (int)__dp4a(ad, ad, 0u);
         if (ref > a.far_thr) {
@@ -194,13 +299,14 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
                 const unsigned adq = __vabsdiffu4(Ip, t.x);
                 const float f = __uint_as_float(__dp4a(adq, adq, acc)) - 12582912.0f;  // = dist2 - ref
                 const float w = ex2(fmaf(-a.cr, f, sxl[tx]));
-                nr = fmaf(w, __uint_as_float(t.y), nr);
+                nr = fmaf(w, __uint_as_float(t.y) - cf, nr);
                 dr += w;
             }
             num = fmaf(rfl[ty], nr, num);
             den = fmaf(rfl[ty], dr, den);
         }
-        Dp = (float)s * fast_div(num, den);
+        Dp = (float)s * (cf + fast_div(num, den));
+        }
         disp_hi[((size_t)b * Hh + y) * Wh + x] = Dp;
     }
     if (!a.do_xyz) return;
@@ -276,6 +382,10 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     constexpr int NT = JB_X * JB_Y / NR;
     __shared__ uint2 sT[JB_LW * JB_LH];
     __shared__ unsigned warp_cnt[NT / 32];
+    __shared__ int wlo[NT / 32], whi[NT / 32];
+    // the staged footprint (JB_X P / S + 2R + 1) x (JB_Y JB_RP / S + 2R + 1) fits sT
+    static_assert((JB_X * P) / S + 2 * R + 1 <= JB_LW && (JB_Y * JB_RP + S - 1) / S + 2 * R + 1 <= JB_LH,
+                  "JB_RP / R too large for the staged tap array");
     const int b = blockIdx.z;
     const int Wh = a.W * S, Hh = a.H * S;
     const int x0 = blockIdx.x * (JB_X * P), y0 = blockIdx.y * (JB_Y * JB_RP);
@@ -283,8 +393,9 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     const int lw = min(x0 + JB_X * P - 1, Wh - 1) / S + R - lx0 + 1;
     const int lh = min(y0 + JB_Y * JB_RP - 1, Hh - 1) / S + R - ly0 + 1;
     const uint8_t *G = guide + (size_t)b * Hh * Wh * 3;
-    stage_taps(sT, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, S, Wh, a, NT);
+    stage_taps(sT, wlo, whi, G, disp_lo + (size_t)b * a.H * a.W, lx0, ly0, lw, lh, S, Wh, a, NT);
     __syncthreads();
+    const bool wide = tile_wide(wlo, whi, NT / 32, a);
     const int x = x0 + P * threadIdx.x;
     int cnt = 0;
 #pragma unroll 1
@@ -317,6 +428,13 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         }
         const int e0 = (cy - R - ly0) * lw + (cx - R - lx0);
         const unsigned cen = sT[e0 + R * lw + R].x;
+        const float cf = __uint_as_float(sT[e0 + R * lw + R].y);
+        if (wide && window_wide<R>(sT + e0, lw, cx, cy, a)) {
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+#pragma unroll
+                for (int k = 0; k < P; ++k) Dp[r][k] = jbu_precise_px<R>(sT + e0, lw, Ip[r][k], u0 + k, v0 + r, cx, cy, a);
+        } else {
         int ref[NR][P];
         bool far = false;
 #pragma unroll
@@ -369,7 +487,7 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
 #pragma unroll
             for (int tx = 0; tx < T; ++tx) {
                 const uint2 tp = row[tx];
-                const float dq = __uint_as_float(tp.y);
+                const float dq = __uint_as_float(tp.y) - cf;
                 const f2_t dd = pk2(dq, dq);
 #pragma unroll
                 for (int r = 0; r < NR; ++r)
@@ -403,9 +521,13 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
                 float n0, n1, d0, d1;
                 upk2(num[r][j], n0, n1);
                 upk2(den[r][j], d0, d1);
-                Dp[r][2 * j] = (float)S * fast_div(n0, d0);
-                Dp[r][2 * j + 1] = (float)S * fast_div(n1, d1);
+                Dp[r][2 * j] = (float)S * (cf + fast_div(n0, d0));
+                Dp[r][2 * j + 1] = (float)S * (cf + fast_div(n1, d1));
             }
+        }
+        }
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
             float *dst = disp_hi + ((size_t)b * Hh + yb + r) * Wh + x;
             if (P == 4)
                 *reinterpret_cast<float4 *>(dst) = make_float4(Dp[r][0], Dp[r][1], Dp[r][2], Dp[r][3]);
@@ -500,6 +622,9 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     a.s = s;
     a.cr = (float)(log2e / (2.0 * (double)sigma_r * sigma_r));
     a.far_thr = (int)floor(4.0 / (double)a.cr);  // reference the minimum when cr * dist2 > ~4
+    a.spread_max = 256.0f;
+    a.cs2 = cs;
+    a.cr2 = log2e / (2.0 * (double)sigma_r * sigma_r);
     // spatial tables (R-15): sub-position u of a footprint has p_down - c = (u + 0.5)/s - 0.5
     for (int u = 0; u < s; ++u) {
         const double f = (u + 0.5) / s - 0.5;

@@ -304,6 +304,44 @@ def test_jbu_far_pixels_vector_equals_scalar_and_oracle(s, r):
     assert np.max(np.abs(vec.reshape(ref.shape).cpu().numpy().astype(np.float64) - ref)) <= 1e-4
 
 
+def _jbu_tol(ref):
+    """include/vsbp.h jbu_upsample_batch: 1e-4 full-res px, or one f32 ulp of the
+    output where that is coarser (outputs >= 2048 px cannot be stored closer)."""
+    return np.maximum(1e-4, np.spacing(np.abs(ref).astype(np.float32)).astype(np.float64))
+
+
+@pytest.mark.parametrize("s,r", [(8, 1), (8, 3), (16, 1), (16, 3), (4, 2), (2, 3)])
+@pytest.mark.parametrize("labels", ["random511", "smooth_high", "steps"])
+def test_jbu_whole_label_domain(s, r, labels):
+    """the tolerance over the whole accepted domain -- labels up
+    to 511 at s = 8 and 16 (outputs to ~8000 px).  Random labels put every window on
+    the precise (double) path; a smooth high ramp keeps the fast f32 path with large
+    outputs (residual accumulation); label steps mix both inside one tile.  Vector
+    and scalar kernels stay bit-identical."""
+    rng = np.random.default_rng(17 * s + r + len(labels))
+    H, W = 15, 23
+    if labels == "random511":
+        lo_np = rng.integers(0, 512, size=(H, W)).astype(np.int32)
+    elif labels == "smooth_high":
+        lo_np = (480 + (np.arange(W)[None, :] + np.arange(H)[:, None]) // 4).astype(np.int32)
+        lo_np = np.minimum(lo_np, 511)
+    else:
+        lo_np = np.where(np.arange(W)[None, :] < W // 2, 3, 505).repeat(H, axis=0).astype(np.int32)
+        lo_np[H // 2:] += rng.integers(0, 3, size=(H - H // 2, W)).astype(np.int32)
+    guide = synthgen.value_noise_rgb(s * r + 5, W * s, H * s)
+    lo, gd = to_dev(lo_np), to_dev(guide)
+    vec = P.jbu_upsample(lo, gd, s, 0.9 * s, 15.0, r)
+    buf = torch.empty(H * s * W * s + 1, dtype=torch.float32, device=dev())
+    sca = P.jbu_upsample(lo, gd, s, 0.9 * s, 15.0, r, out=buf[1:].view(1, H * s, W * s))
+    assert torch.equal(vec.reshape(sca.shape), sca)
+    ref = oracle.jbu(lo_np, guide, s, 0.9 * s, 15.0, r)
+    got = vec.reshape(ref.shape).cpu().numpy().astype(np.float64)
+    err = np.abs(got - ref)
+    assert (err <= _jbu_tol(ref)).all(), (err.max(), ref.flat[np.argmax(err)])
+    below = np.abs(ref) < 2048
+    assert err[below].max(initial=0.0) <= 1e-4
+
+
 def test_jbu_full_frame_config3():
     left, _, d_lo = synthgen.stereo_pair_rgb(2)
     got = P.jbu_upsample(to_dev(d_lo), to_dev(left), 4, 3.75, 15.0, 2).cpu().numpy().astype(np.float64)
