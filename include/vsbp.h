@@ -180,6 +180,40 @@ int reproject(const float *disp, int W, int H, const double *Q, float min_disp, 
               unsigned long long *n_valid, void *stream);
 
 /* ---------------------------------------------------------------------------
+ * vsbp_q_matrix -- Eq.3 as the 4x4 matrix reproject* take, with the
+ * printed z = (B/d)(f B/du) read as z = f_du B / d (R-20, the only form that
+ * inverts Eq.3's first line):
+ *   Q = [[1, 0, 0, -u0], [0, f_du/f_dv, 0, -v0 f_du/f_dv], [0, 0, 0, f_du],
+ *        [0, 0, 1/B, 0]]   (row-major, written to the HOST double[16] Q)
+ * so that x = B(u-u0)/d, y = B(v-v0)(f_du/f_dv)/d, z = f_du B/d.  f_du, f_dv, B
+ * must be finite and nonzero (else VSBP_EINVAL).  Host-only.
+ * ------------------------------------------------------------------------- */
+int vsbp_q_matrix(double f_du, double f_dv, double u0, double v0, double B, double *Q);
+
+/* ---------------------------------------------------------------------------
+ * compact_cloud_batch -- a8, the per-pair point cloud as PACKED valid points in
+ * raster order (Eq.3 turns each pair's disparity into "a point cloud";
+ * SURVEY 8(a) a8; R-20, R-21):
+ *   disp      : float [B][H][W] full-res disparity (px), device
+ *   Q         : HOST double[16] (as reproject_batch); min_disp > 0
+ *   xyz       : float [cap_points][3] device output: the points with
+ *               d >= min_disp, pair-major then row-major then column-major, each
+ *               bit-identical to reproject's / jbu_reproject_batch's entry
+ *   offsets   : device int64 [B+1]: offsets[b] = index of pair b's first point,
+ *               offsets[B] = total points (always exact, even past cap_points)
+ *   n_valid   : device uint64 [B], overwritten with each pair's count
+ *   workspace : device scratch of compact_workspace_bytes(B, W, H) bytes
+ * Points at index >= cap_points are not written (cap_points = B*W*H can never
+ * overflow).  One single-pass kernel (decoupled look-back scan); async.
+ * Errors: VSBP_EINVAL (null pointers, B < 1, W*H > 2^30, min_disp <= 0, workspace
+ * too small, cap_points < 0).
+ * ------------------------------------------------------------------------- */
+size_t compact_workspace_bytes(int B, int W, int H);
+int compact_cloud_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+                        long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
+                        size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
  * prep_downsample_batch -- a0 (R-22): for n frames,
  *   rgb_hi : u8 [n][H_hi][W_hi][3]  ->  gray_lo : u8 [n][H_hi/s][W_hi/s]
  *   grey = (77R+150G+29B+128)>>8, then s x s mean rounded half up.

@@ -78,6 +78,7 @@ def lib():
         L.oracle_jbu.argtypes = [p, i, i, p, i, dbl, dbl, i, p]
         L.oracle_reproject.argtypes = [p, i, i, p, dbl, p, p]
         L.oracle_disp_summary.argtypes = [p, i, i, p, p]
+        L.oracle_compact_cloud.argtypes = [p, i, i, p, dbl, p, p]
         for name in ("oracle_quantize", "oracle_prep", "oracle_cost_volume", "oracle_pyramid_down",
                      "oracle_message", "oracle_bp_level", "oracle_upcopy", "oracle_wta",
                      "oracle_bp_disparity", "oracle_jbu", "oracle_reproject", "oracle_disp_summary"):
@@ -368,6 +369,18 @@ def reproject(disp: np.ndarray, Q: np.ndarray, min_disp: float = 1.0):
     _check(lib().oracle_reproject(_ptr(disp), W, H, _ptr(Q), min_disp, _ptr(xyz), _ptr(n)),
            "oracle_reproject")
     return xyz, int(n[0])
+
+
+def compact_cloud(disp: np.ndarray, Q: np.ndarray, min_disp: float = 1.0) -> np.ndarray:
+    """a8 (R-21): the valid points of Eq.3 in raster order, double [n][3]."""
+    disp = np.ascontiguousarray(disp, np.float64)
+    Q = np.ascontiguousarray(Q, np.float64).reshape(16)
+    H, W = disp.shape
+    xyz = np.zeros((H * W, 3), np.float64)
+    n = np.zeros(1, np.int64)
+    _check(lib().oracle_compact_cloud(_ptr(disp), W, H, _ptr(Q), min_disp, _ptr(xyz), _ptr(n)),
+           "oracle_compact_cloud")
+    return xyz[: int(n[0])].copy()
 
 
 def disp_summary(disp: np.ndarray):

@@ -485,6 +485,36 @@ int oracle_reproject(const double *disp, int W, int H, const double *Q, double m
 }
 
 /* ------------------------------------------------------------------------- */
+/* a8  compaction: the pair's point cloud as the list of valid points in raster */
+/*     order ("a point cloud"; R-21 validity).  For v = 0..H-1, u = 0..W-1: */
+/*     if disp(u,v) >= min_disp, append (X,Y,Z)/Wh of Q [u v d 1]^T (Eq.3).      */
+/*     xyz has room for W*H points; *n = the number appended.                   */
+/* ------------------------------------------------------------------------- */
+int oracle_compact_cloud(const double *disp, int W, int H, const double *Q, double min_disp, double *xyz,
+                         int64_t *n)
+{
+    if (!disp || !Q || !xyz || !n || W < 1 || H < 1) return OR_EINVAL;
+    if (!(min_disp > 0.0)) return OR_EINVAL;
+    int64_t k = 0;
+    for (int v = 0; v < H; ++v)
+        for (int u = 0; u < W; ++u) {
+            double d = disp[(size_t)v * W + u];
+            if (!(d >= min_disp)) continue;
+            double in[4] = {(double)u, (double)v, d, 1.0}, out[4];
+            for (int r = 0; r < 4; ++r) {
+                out[r] = 0.0;
+                for (int c = 0; c < 4; ++c) out[r] += Q[4 * r + c] * in[c];
+            }
+            xyz[3 * k] = out[0] / out[3];
+            xyz[3 * k + 1] = out[1] / out[3];
+            xyz[3 * k + 2] = out[2] / out[3];
+            ++k;
+        }
+    *n = k;
+    return OR_OK;
+}
+
+/* ------------------------------------------------------------------------- */
 /* a8  per-pair summary: label sum and an order-independent    */
 /* 64-bit hash of the low-res disparity, hash = sum_i mix(i << 32 | label_i)    */
 /* mod 2^64, mix = SplitMix64 finaliser.                                       */

@@ -90,6 +90,10 @@ _EXPORTS = {
                                      C.c_void_p, C.c_void_p]),
     "bp_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "bp_timing_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "vsbp_q_matrix": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_void_p]),
+    "compact_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "compact_cloud_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p,
+                                      C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vsbp_strerror": (C.c_char_p, [C.c_int]),
     "vsbp_launch_count": (C.c_uint64, []),
 }
@@ -388,11 +392,12 @@ def icp_register(src: torch.Tensor, tgt: torch.Tensor, init=None, max_iter: int 
 
 
 def q_matrix(f_du: float, f_dv: float, u0: float, v0: float, B: float) -> np.ndarray:
-    """Eq.3 as a 4x4 reprojection matrix with z = f B/(d du) (R-20)."""
-    return np.array([[1.0, 0.0, 0.0, -u0],
-                     [0.0, f_du / f_dv, 0.0, -v0 * f_du / f_dv],
-                     [0.0, 0.0, 0.0, f_du],
-                     [0.0, 0.0, 1.0 / B, 0.0]], dtype=np.float64)
+    """Eq.3 as a 4x4 reprojection matrix with z = f B/(d du) (R-20),
+    built by the library's vsbp_q_matrix."""
+    Q = np.zeros(16, np.float64)
+    _check(lib().vsbp_q_matrix(float(f_du), float(f_dv), float(u0), float(v0), float(B),
+                               Q.ctypes.data_as(C.c_void_p)), "vsbp_q_matrix")
+    return Q.reshape(4, 4)
 
 
 def reproject(disp: torch.Tensor, Q, min_disp: float = 1.0, xyz: torch.Tensor | None = None,
@@ -438,6 +443,40 @@ def jbu_reproject(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_
                                      _dev(xyz, torch.float32, "xyz"), _dev(n_valid, torch.int64, "n_valid"),
                                      _stream(stream)), "jbu_reproject_batch")
     return disp_hi, xyz, n_valid
+
+
+class CloudCompactor:
+    """a8: packed point clouds (compact_cloud_batch).  Owns the look-back workspace
+    for batches up to ``batch`` pairs of W x H disparity maps."""
+
+    def __init__(self, W: int, H: int, batch: int, device="cuda"):
+        self.W, self.H, self.batch = W, H, batch
+        n = int(lib().compact_workspace_bytes(batch, W, H))
+        self.workspace = torch.empty(n, dtype=torch.uint8, device=device)
+
+    def __call__(self, disp: torch.Tensor, Q, min_disp: float = 1.0, xyz: torch.Tensor | None = None,
+                 offsets: torch.Tensor | None = None, n_valid: torch.Tensor | None = None, stream=None):
+        """disp float32 [B,H,W] -> (xyz float32 [cap,3] packed, offsets int64 [B+1], n_valid int64 [B]).
+        Pair b's points are xyz[offsets[b]:offsets[b+1]] in raster order."""
+        if disp.dim() == 2:
+            disp = disp.unsqueeze(0)
+        B, H, W = disp.shape
+        if (W, H) != (self.W, self.H) or B > self.batch:
+            raise ValueError("disparity shape does not match the compactor")
+        dev = disp.device
+        if xyz is None:
+            xyz = torch.empty((B * H * W, 3), dtype=torch.float32, device=dev)
+        if offsets is None:
+            offsets = torch.empty(B + 1, dtype=torch.int64, device=dev)
+        if n_valid is None:
+            n_valid = torch.empty(B, dtype=torch.int64, device=dev)
+        Qh = np.ascontiguousarray(np.asarray(Q, np.float64).reshape(16))
+        _check(lib().compact_cloud_batch(B, _dev(disp, torch.float32, "disp"), W, H, Qh.ctypes.data_as(C.c_void_p),
+                                         min_disp, _dev(xyz, torch.float32, "xyz"), xyz.shape[0],
+                                         _dev(offsets, torch.int64, "offsets"), _dev(n_valid, torch.int64, "n_valid"),
+                                         C.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
+                                         _stream(stream)), "compact_cloud_batch")
+        return xyz, offsets, n_valid
 
 
 SUMMARY_BYTES = 64

@@ -586,6 +586,38 @@ int jbu_upsample(const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb,
     return jbu_upsample_batch(1, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, stream);
 }
 
+int vsbp_q_matrix(double f_du, double f_dv, double u0, double v0, double B, double *Q)
+{
+    if (!Q || !std::isfinite(f_du) || !std::isfinite(f_dv) || !std::isfinite(u0) || !std::isfinite(v0) ||
+        !std::isfinite(B) || f_du == 0.0 ||
+        f_dv == 0.0 || B == 0.0)
+        return VSBP_EINVAL;
+    const double r = f_du / f_dv;
+    const double q[16] = {1.0, 0.0, 0.0, -u0, 0.0, r, 0.0, -v0 * r, 0.0, 0.0, 0.0, f_du, 0.0, 0.0, 1.0 / B, 0.0};
+    for (int i = 0; i < 16; ++i) Q[i] = q[i];
+    return VSBP_OK;
+}
+
+size_t compact_workspace_bytes(int B, int W, int H)
+{
+    if (B < 1 || W < 1 || H < 1) return 0;
+    return vsbp::compact_workspace_bytes(B, W, H);
+}
+
+int compact_cloud_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
+                        long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
+                        size_t ws_bytes, void *stream)
+{
+    if (B < 1 || !disp || !Q || !xyz || !offsets || !n_valid || !workspace || W < 1 || H < 1) return VSBP_EINVAL;
+    if ((long long)W * H > (1ll << 30) || !(min_disp > 0.f) || cap_points < 0) return VSBP_EINVAL;
+    if (ws_bytes < vsbp::compact_workspace_bytes(B, W, H) || ((uintptr_t)workspace & 7)) return VSBP_EINVAL;
+    float Qf[16];
+    for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
+    CK(vsbp::launch_compact(B, disp, W, H, Qf, min_disp, xyz, cap_points, offsets, n_valid, workspace,
+                            (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
 int reproject_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
                     unsigned long long *n_valid, void *stream)
 {

@@ -68,6 +68,11 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
 cudaError_t launch_reproject(int B, const float *disp, int W, int H, const float Qf[16], float min_disp, float *xyz,
                              unsigned long long *n_valid, cudaStream_t st);
 cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray, cudaStream_t st);
+// a8 compaction (compact.cu)
+size_t compact_workspace_bytes(int B, int W, int H);
+cudaError_t launch_compact(int B, const float *disp, int W, int H, const float Qf[16], float min_disp, float *xyz,
+                           long long cap, long long *offsets, unsigned long long *n_valid, void *ws,
+                           cudaStream_t st);
 cudaError_t launch_summary(int B, const int32_t *disp, int W, int H, const unsigned long long *n_valid,
                            uint64_t first_pair_id, void *summary, cudaStream_t st);
 

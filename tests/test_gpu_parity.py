@@ -740,3 +740,93 @@ def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters, variant):
         bp.messages(0, 0)
     if levels > 1:
         bp.messages(0, 1)  # coarser levels are still materialised
+
+
+# ----------------------------------------------------------------------------- a8 compaction
+def _check_compaction(disp_np, Q, min_disp=1.0, batch=None):
+    """compact_cloud_batch vs oracle.compact_cloud fed the same f32 disparities:
+    exact counts and offsets (the validity test sees the same f32 value on both
+    sides), every point within 1e-5 relative, raster order per pair."""
+    B, H, W = disp_np.shape
+    comp = P.CloudCompactor(W, H, batch or B, device=dev())
+    xyz, off, nv = comp(to_dev(disp_np.astype(np.float32)), Q, min_disp)
+    torch.cuda.synchronize()
+    off = off.cpu().numpy()
+    nv = nv.cpu().numpy()
+    xyz = xyz.cpu().numpy().astype(np.float64)
+    ref = [oracle.compact_cloud(disp_np[b].astype(np.float32).astype(np.float64), Q, min_disp) for b in range(B)]
+    counts = np.array([r.shape[0] for r in ref])
+    assert np.array_equal(nv, counts)
+    assert np.array_equal(off, np.concatenate([[0], np.cumsum(counts)]))
+    for b in range(B):
+        got = xyz[off[b]:off[b + 1]]
+        if counts[b]:
+            err = np.linalg.norm(got - ref[b], axis=1) / np.linalg.norm(ref[b], axis=1)
+            assert err.max() <= 1e-5, (b, err.max())
+    return xyz, off
+
+
+@pytest.mark.parametrize("B,W,H,frac", [(1, 7, 5, 0.5), (3, 45, 91, 0.7), (2, 2048, 1, 0.9), (5, 3, 700, 0.2),
+                                        (4, 173, 61, 0.0), (2, 64, 64, 1.0), (9, 301, 17, 0.5)])
+def test_compact_cloud_matches_oracle(B, W, H, frac):
+    """Ragged tiles (W*H not a multiple of the 2048-pixel tile), W < the 8 pixels a
+    thread owns, empty and full pairs, tile boundaries inside rows."""
+    rng = np.random.default_rng(B * W + H)
+    d = rng.uniform(1.0, 200.0, size=(B, H, W))
+    d[rng.random((B, H, W)) >= frac] = rng.uniform(-5.0, 0.999)
+    Q = oracle.q_matrix(900.0, 880.0, W / 2, H / 2, 0.5)
+    _check_compaction(d, Q)
+
+
+def test_compact_cloud_equals_dense_jbu_cloud_and_caps():
+    """A packed point is bit-identical to the fused JBU+reprojection kernel's dense
+    entry (same f32 Eq.3); points past cap_points are not written while offsets
+    stay exact; repeated runs are deterministic."""
+    s, r = 4, 2
+    left, _, d_lo = synthgen.stereo_pair_rgb(4, 512, 256, s, 8, 48)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(700.0, 700.0, 255.5, 127.5, I["B"])
+    lo = to_dev(np.stack([d_lo, d_lo[::-1].copy()]))
+    gd = to_dev(np.stack([left, left[::-1].copy()]))
+    hi, dense, n = P.jbu_reproject(lo, gd, s, 3.75, 15.0, r, Q, 3.0 * s)
+    comp = P.CloudCompactor(512, 256, 2, device=dev())
+    xyz, off, nv = comp(hi, Q, 3.0 * s)
+    torch.cuda.synchronize()
+    assert torch.equal(nv, n.to(torch.int64))
+    valid = ~torch.isnan(dense[..., 0])
+    assert torch.equal(xyz[: int(off[-1])], dense[valid])
+    xyz2, off2, _ = comp(hi, Q, 3.0 * s)
+    assert torch.equal(xyz2[: int(off2[-1])], xyz[: int(off[-1])]) and torch.equal(off, off2)
+    cap = int(off[1]) + 17
+    small = torch.full((cap + 5, 3), 7.0, device=dev())
+    xs, offs, _ = comp(hi, Q, 3.0 * s, xyz=small[:cap])
+    torch.cuda.synchronize()
+    assert torch.equal(offs, off)
+    assert torch.equal(xs[:cap], xyz[:cap]) and bool((small[cap:] == 7.0).all())
+
+
+def test_compact_cloud_full_frames_sampled():
+    """BASELINE C3 size (2704 x 1520, 3 pairs, JBU output of the bench path):
+    counts / offsets exact, sampled points vs the oracle."""
+    left, right, d_lo = synthgen.stereo_pair_rgb(6)
+    I = synthgen.INTRINSICS
+    Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
+    lo = to_dev(np.stack([d_lo, d_lo, d_lo]))
+    gd = to_dev(np.stack([left, left[:, ::-1].copy(), left[::-1].copy()]))
+    hi = P.jbu_upsample(lo, gd, 4, 3.75, 15.0, 2)
+    hi[1, :100] = 0.0  # an invalid band
+    comp = P.CloudCompactor(2704, 1520, 3, device=dev())
+    xyz, off, nv = comp(hi, Q, 1.0)
+    torch.cuda.synchronize()
+    hi_np = hi.cpu().numpy()
+    counts = (hi_np >= 1.0).reshape(3, -1).sum(axis=1)
+    assert np.array_equal(nv.cpu().numpy(), counts)
+    assert np.array_equal(off.cpu().numpy(), np.concatenate([[0], np.cumsum(counts)]))
+    rng = np.random.default_rng(0)
+    xyz = xyz.cpu().numpy().astype(np.float64)
+    for b in range(3):
+        ref = oracle.compact_cloud(hi_np[b].astype(np.float64), Q, 1.0)
+        idx = rng.integers(0, counts[b], size=2000)
+        got = xyz[off.cpu().numpy()[b] + idx]
+        err = np.linalg.norm(got - ref[idx], axis=1) / np.linalg.norm(ref[idx], axis=1)
+        assert err.max() <= 1e-5

@@ -489,6 +489,36 @@ def test_reproject_round_trip():
 
 
 # ----------------------------------------------------------------------------- a8
+def test_compact_cloud_raster_order_round_trip():
+    """a8 compaction (R-21): points constructed in 3-D and projected with the
+    FIRST line of Eq.3 come back from the packed cloud in raster order
+    (v, then u) to 1e-9; the packed list equals the dense reprojection's non-NaN
+    rows; nothing valid -> no points; min_disp <= 0 rejected."""
+    I = synthgen.INTRINSICS
+    Q = oracle.q_matrix(I["f_du"], 1390.0, I["u0"], I["v0"], I["B"])
+    rng = np.random.default_rng(12)
+    H, W = 31, 47
+    disp = np.where(rng.random((H, W)) < 0.3, 0.5, 0.0)  # invalid background (d < 1)
+    pts = {}
+    for _ in range(300):
+        u, v = int(rng.integers(0, W)), int(rng.integers(0, H))
+        z = float(rng.uniform(5, 200))
+        x = (u - I["u0"]) * z / I["f_du"]
+        y = (v - I["v0"]) * z / 1390.0
+        disp[v, u] = project((x, y, z), I["f_du"], 1390.0, I["u0"], I["v0"], I["B"])[2]
+        pts[(v, u)] = (x, y, z)
+    got = oracle.compact_cloud(disp, Q, 1.0)
+    want = np.array([pts[k] for k in sorted(pts)])
+    assert got.shape == want.shape
+    assert np.allclose(got, want, rtol=1e-9, atol=1e-9)
+    dense, n = oracle.reproject(disp, Q, 1.0)
+    assert n == got.shape[0]
+    assert np.array_equal(got, dense[~np.isnan(dense[..., 0])])
+    assert oracle.compact_cloud(np.zeros((4, 5)), Q, 1.0).shape == (0, 3)
+    with pytest.raises(oracle.OracleError):
+        oracle.compact_cloud(disp, Q, 0.0)
+
+
 def test_disp_summary_hash_known_value():
     # SplitMix64 seeded with 0 yields 0xE220A8397B1DCDAF as its first output,
     # which is mix(0) here: one pixel at index 0 with label 0.
