@@ -4,17 +4,22 @@
 Contract (driver): `python bench.py --gpus N --steps K --warmup W [--impl reference]`,
 torchrun for N > 1 (one rank per GPU, NCCL).  Rank 0 prints ONE JSON line.
 
-Workload (BASELINE.json configs[4], the metric's configuration, per GPU): a stream
-of synthetic 2.7K RGB virtual-stereo pairs; one step = one batch of B pairs per
-GPU through the whole path: prep (s=4) -> hierarchical BP 676x380, L=64, 5 levels
-x 5 iterations -> JBU r=2 to 2704x1520 -> reprojection -> per-pair summary, then
-an NCCL all_gather of the summaries (the only exchange).  Pairs are
-sharded round-robin by batch (batch k of B pairs -> rank k mod N, shard.py): weak scaling.
+Workload (BASELINE.json configs[4], the metric's configuration): a stream of 4096
+virtual-stereo pairs of a synthetic 2.7K UAV video (synthgen/video.py, rendered
+on the device by synthgen/libsynth.so before timing), pair k = (frame k, frame
+k+1), so every frame is shared by two pairs.  One step =
+one batch of B pairs (B+1 frames) per GPU through the whole path: prep (s=4) ->
+hierarchical BP 676x380, L=64, 5 levels x 5 iterations -> JBU r=2 to 2704x1520
+-> packed point clouds (Eq.3 + raster-order compaction) -> per-pair summary,
+then the all_gather of the summaries on a side stream (the only exchange, SURVEY
+§8e).  Batches go round-robin to the ranks (batch g -> rank g mod N, shard.py):
+weak scaling; a rank cycles over its share of the stream.
 
 `value`  : pairs/s over all ranks, inputs resident in HBM, device-timed (CUDA
            events on the launching stream, max over ranks).
-`e2e`    : the same through the public API with pinned HOST frames, H2D of the
-           step's RGB pairs and D2H of its summaries inside the timed region.
+`e2e`    : the same through the public API (StereoStream) with pinned HOST frame
+           batches, the H2D of each step's B+1 frames and the D2H of its
+           (gathered) summaries inside the timed region.
 `roofline`: the dominant kernel (level-0 message updates, a4): algorithmic bytes
            / device time from live CUDA events inside the timed region, against
            MEASURED_PEAKS.json hbm_gbs.
@@ -41,8 +46,9 @@ METRIC = "2.7K frame pairs/sec (disparity+point cloud) at 1/2/4/8 B200; HBM GB/s
 W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS = 2704, 1520, 4, 64, 5, 5
 FEATURES = dict(gc=30, gr=30, K=4, thr=10 ** 9, r=5, sr=48)  # f3 on the 676x380 grey pair (P:84 grid)
 CAMERA = (1400.0, 1400.0, 1351.5, 759.5, -0.25, 0.08, -0.01)  # f1: GoPro-like radial model
-WORKLOAD = ("C5 per GPU: stream of synthetic 2.7K RGB pairs, full pipeline a0-a8 "
-            "(prep s=4 -> BP 676x380 L=64 5 levels x 5 iters -> JBU r=2 to 2704x1520 -> reproject -> summary)")
+WORKLOAD = ("C5: stream of 4096 virtual-stereo pairs of a synthetic 2.7K video (pair k = frames k, k+1), full "
+            "pipeline a0-a8 (prep s=4 -> BP 676x380 L=64 5 levels x 5 iters -> JBU r=2 to 2704x1520 -> Eq.3 + "
+            "packed point cloud -> summary -> gather)")
 
 
 def parse():
@@ -52,7 +58,8 @@ def parse():
     p.add_argument("--warmup", type=int, default=5)
     p.add_argument("--batch", type=int, default=128,
                    help="pairs per GPU per step (measured: 32 / 64 / 96 / 128 / 160 -> 6865 / 7041 / 7102 / 7135 / 7127 pairs/s)")
-    p.add_argument("--pool", type=int, default=4, help="distinct synthetic pairs generated per rank")
+    p.add_argument("--pairs", type=int, default=4096, help="length of the synthetic stream (C5: 4096 pairs)")
+    p.add_argument("--seed", type=int, default=1902)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -132,14 +139,25 @@ class ClockSampler:
                 "reasons": sorted(reasons)}
 
 
-def make_pool(seed0: int, n: int):
-    import synthgen
-    lefts, rights = [], []
-    for i in range(n):
-        l, r, _ = synthgen.stereo_pair_rgb(seed0 + i, W_HI, H_HI, S_DOWN, 8, 48)
-        lefts.append(l)
-        rights.append(r)
-    return np.stack(lefts), np.stack(rights)
+def video_scene(seed: int):
+    from synthgen.video import VideoScene
+    return VideoScene(seed, W_HI, H_HI, S_DOWN, 8, 48)  # C2/C3 label range [8, 48] of L = 64
+
+
+def host_frames(seed: int, k0: int, n: int):
+    """n consecutive frames of the video as numpy (device generator when a GPU is
+    present; the bit-identical numpy twin otherwise, ~15 s per frame)."""
+    from synthgen import video
+    sc = video_scene(seed)
+    try:
+        import torch
+        if torch.cuda.is_available():
+            out = torch.empty((n, H_HI, W_HI, 3), dtype=torch.uint8, device="cuda")
+            video.frames_device(sc, k0, out)
+            return out.cpu().numpy()
+    except ImportError:
+        pass
+    return np.stack([sc.frame(k0 + i) for i in range(n)])
 
 
 def q_intrinsics():
@@ -165,17 +183,19 @@ def ncu_traffic(batch: int):
 
 
 # ----------------------------------------------------------------------------- oracle timing
-def oracle_rate(n_threads: int, pairs_per_thread: int, left, right):
+def oracle_rate(n_threads: int, pairs_per_thread: int, frames):
     """Run the oracle pipeline (a0-a8) on n_threads host threads (ctypes releases the
-    GIL), each on pairs_per_thread pairs; returns (pairs/s, pairs, seconds)."""
+    GIL), each on pairs_per_thread pairs (frames[i], frames[i+1]) of the video;
+    returns (pairs/s, pairs, seconds)."""
     import oracle
     I = q_intrinsics()
     Q = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
 
     def work(k):
         for j in range(pairs_per_thread):
-            i = (k + j) % len(left)
-            oracle.pipeline_pair(left[i], right[i], S_DOWN, NDISP, LEVELS, ITERS, Q)
+            i = (k + j) % (len(frames) - 1)
+            d, hi, xyz, n = oracle.pipeline_pair(frames[i], frames[i + 1], S_DOWN, NDISP, LEVELS, ITERS, Q)
+            oracle.compact_cloud(hi, Q, 1.0)  # a8: the packed cloud, as the GPU path
 
     ts = [threading.Thread(target=work, args=(k,)) for k in range(n_threads)]
     t0 = time.perf_counter()
@@ -204,12 +224,12 @@ def run_reference(args):
     import oracle
     oracle.build()
     threads = args.cpu_threads or default_threads()
-    left, right = make_pool(1000, min(args.pool, threads))
+    frames = host_frames(args.seed, 0, threads + 1)
     for _ in range(args.warmup):  # untimed rounds
-        oracle_rate(threads, 1, left, right)
+        oracle_rate(threads, 1, frames)
     times, pairs = 0.0, 0
     for _ in range(args.steps):
-        _, n, dt = oracle_rate(threads, 1, left, right)
+        _, n, dt = oracle_rate(threads, 1, frames)
         times += dt
         pairs += n
     v = pairs / times
@@ -219,7 +239,8 @@ def run_reference(args):
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "int32",
         "data": "synthetic", "config": {"workload": WORKLOAD, "pairs_per_step": threads},
         "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
-                         "sample": f"{threads} pairs per step (one per host thread), {args.steps} steps"},
+                         "sample": f"{threads} pairs per step (one per host thread, consecutive frames of the "
+                                   f"C5 video), {args.steps} steps"},
         "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -234,12 +255,15 @@ def run_ours(args):
     import paper_1902_09733_b200 as P
     from paper_1902_09733_b200 import shard
 
-    rank, world, local = dist_env()
+    rank, world, local_rank = dist_env()
     if world != args.gpus:
         raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    torch.cuda.set_device(local_rank)
+    dev = torch.device("cuda", local_rank)
     if world > 1:
+        # keep NCCL's communicator-init lines in the log (the driver's rank check reads them)
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
         dist.init_process_group("nccl", device_id=dev)
     P.lib()
     B = args.batch
@@ -252,20 +276,34 @@ def run_ours(args):
     if full_bp:
         pipe.bp.timing(True)
 
-    # seeded synthetic pairs; rank r owns global batches r, r+N, ... (shard.py)
-    pool_n = max(1, min(args.pool, B))
-    lpool, rpool = make_pool(7000 + 100 * rank, pool_n)
-    idx = [i % pool_n for i in range(B)]
-    left_h = torch.from_numpy(lpool[idx]).pin_memory()
-    right_h = torch.from_numpy(rpool[idx]).pin_memory()
-    left_d = left_h.to(dev)
-    right_d = right_h.to(dev)
-    gathered = torch.empty((world * B, 8), dtype=torch.int64, device=dev)
+    # the C5 stream: pair k = (frame k, frame k+1) of one synthetic video; rank r owns
+    # global batches r, r+N, ... (shard.py), each B+1 frames, rendered into HBM now
+    from synthgen import video
+    scene = video_scene(args.seed)
+    nbatch = (args.pairs + B - 1) // B
+    local = [g for g in range(nbatch) if g % world == rank] or [rank]
+    frames = torch.empty((len(local), B + 1, H_HI, W_HI, 3), dtype=torch.uint8, device=dev)
+    for li, g in enumerate(local):
+        video.frames_device(scene, g * B, frames[li])
+    torch.cuda.synchronize(dev)
     stream = torch.cuda.current_stream(dev)
+    side = torch.cuda.Stream(device=dev)
+    RING = 4
+    sdev = [torch.empty((B, 8), dtype=torch.int64, device=dev) for _ in range(RING)]
+    gdev = [torch.empty((world * B, 8), dtype=torch.int64, device=dev) for _ in range(RING)]
+    produced = [torch.cuda.Event() for _ in range(RING)]
+    consumed = [torch.cuda.Event() for _ in range(RING)]
 
-    def step(s, lt, rt):
-        summ = pipe.run(lt, rt, first_pair_id=shard.batch_first_pair(s, rank, world, B))
-        shard.gather_summaries(summ, out=gathered)  # the one exchange
+    def step(s):
+        li = s % len(local)
+        r = s % RING
+        stream.wait_event(consumed[r])
+        summ = pipe.run_frames(frames[li], first_pair_id=local[li] * B, summary_out=sdev[r])
+        produced[r].record(stream)
+        with torch.cuda.stream(side):  # the one exchange, off the compute stream
+            side.wait_event(produced[r])
+            shard.gather_summaries(summ, out=gdev[r])
+            consumed[r].record(side)
         return summ
 
     def barrier():
@@ -281,12 +319,12 @@ def run_ours(args):
         return float(t.item())
 
     for s in range(args.warmup):
-        step(s, left_d, right_d)
+        step(s)
     if full_bp:
         pipe.bp.timing_read()  # discard warm-up timings
     barrier()
 
-    sampler = ClockSampler(local)
+    sampler = ClockSampler(local_rank)
     sampler.start()
     time.sleep(0.3)
     n0 = P.launch_count()
@@ -294,7 +332,8 @@ def run_ours(args):
     barrier()
     e0.record(stream)
     for s in range(args.steps):
-        step(args.warmup + s, left_d, right_d)
+        step(args.warmup + s)
+    stream.wait_stream(side)
     e1.record(stream)
     barrier()
     launches = P.launch_count() - n0
@@ -304,30 +343,36 @@ def run_ours(args):
     lv = pipe.bp.timing_read() if full_bp else None
     pairs = world * B * args.steps
     value = pairs / (ms_max / 1000.0)
+    n_valid_last = int(pipe.offsets[B].item()) if pipe.offsets is not None else None
 
-    # ---- e2e: pinned host frames in, summaries out, through the public API
+    # ---- e2e: pinned host frame batches in, summaries out, through the public API
     e2e = None
     if not args.no_e2e:
-        # public API end to end: pinned host pairs -> StereoStream (H2D of batch i+1
-        # overlapped with compute of batch i) -> summaries back in pinned host memory
-        runner = P.StereoStream(pipe, device=dev)
-        runner.run([(left_h, right_h)] * 2)  # warm the copy path
+        runner = P.StereoStream(pipe, device=dev, ring=RING, world=world)
+        hb = [frames[i % len(local)].cpu().pin_memory() for i in range(2)]  # two distinct host batches
+        gather = (lambda summ, out: shard.gather_summaries(summ, out=out))
+        got = []
+        runner.run(hb, gather=gather)  # warm the copy path
         barrier()
+        runner.h2d_bytes = runner.d2h_bytes = 0
         f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         f0.record(stream)
-        gather = (lambda summ: shard.gather_summaries(summ, out=gathered)) if world > 1 else None
-        runner.run([(left_h, right_h)] * args.steps, first_pair_id=shard.batch_first_pair(0, rank, world, B),
-                   pair_stride=world * B, gather=gather)
+        runner.run([hb[i & 1] for i in range(args.steps)], first_pair_id=shard.batch_first_pair(0, rank, world, B),
+                   pair_stride=world * B, gather=gather, on_summary=lambda i, t: got.append(i))
         f1.record(stream)
         barrier()
+        assert got == list(range(args.steps)), "a batch's summaries never reached the host"
         ems = max_over_ranks(f0.elapsed_time(f1))
         e2e = {"value": pairs / (ems / 1000.0), "unit": "pairs/s",
-               "h2d_gbs_per_gpu": args.steps * (left_h.numel() + right_h.numel()) / (ems / 1000.0) / 1e9,
-               "h2d_bytes_per_step": int(left_h.numel() + right_h.numel()),
-               "d2h_bytes_per_step": int(runner.summary_host.numel() * 8),
-               "overlap": "H2D of batch i+1 on a copy stream during compute of batch i"}
+               "h2d_gbs_per_gpu": runner.h2d_bytes / (ems / 1000.0) / 1e9,
+               "h2d_bytes_per_step": int(runner.h2d_bytes // args.steps),
+               "d2h_bytes_per_step": int(runner.d2h_bytes // args.steps),
+               "h2d_bytes_per_pair": runner.h2d_bytes / (args.steps * B),
+               "overlap": "H2D of batch i+1 on a copy stream during compute of batch i; gather + D2H of the "
+                          "summaries on a side stream"}
         if full_bp:
             pipe.bp.timing_read()
+        del hb
 
     # ---- roofline of the dominant kernel: level-0 message updates (a4)
     peak, peak_kind = measured_peaks()
@@ -351,9 +396,11 @@ def run_ours(args):
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         threads = args.cpu_threads or default_threads()
-        v, n, dt = oracle_rate(threads, args.cpu_pairs, lpool, rpool)
+        fr = frames[0, : min(threads, B) + 1].cpu().numpy()
+        v, n, dt = oracle_rate(threads, args.cpu_pairs, fr)
         cpu = {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
-               "sample": f"{n} pairs of the same workload, one per host thread ({dt:.1f} s)"}
+               "sample": f"{n} pairs of the same workload (consecutive frames of the C5 video), one thread per "
+                         f"pair at a time ({dt:.1f} s)"}
 
     if rank == 0:
         line = {
@@ -365,13 +412,17 @@ def run_ours(args):
                        + (f" with f2 constant-space BP (k0={args.csbp})" if args.csbp else ""),
                        "batch_per_gpu": B, "pairs_per_step": world * B,
                        "parallelism": f"dp{world} (pairs round-robin, NCCL all_gather of summaries)",
-                       "l2": f"inputs larger than L2 ({(left_d.numel() + right_d.numel()) / 1e6:.0f} MB RGB + "
-                             f"{pipe.bp.workspace.numel() / 1e6:.0f} MB BP state per step)",
+                       "stream_pairs": nbatch * B, "frames_in_hbm": int(frames.shape[0] * frames.shape[1]),
+                       "frames_per_step": B + 1, "cloud": "packed (raster-order valid points, offsets per pair)",
+                       "l2": f"inputs larger than L2 ({frames[0].numel() / 1e6:.0f} MB RGB + "
+                             f"{pipe.bp.workspace.numel() / 1e6:.0f} MB BP state per step, a different batch "
+                             f"of the stream every step)",
                        "bp_msg_storage": f"u{8 * pipe.bp.params()['msg_bytes']}" if full_bp else "i32 (csbp)",
                        "jbu_arith": "f32"},
             "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
             "cpu_baseline": cpu,
             "per_level_update_ms_per_step": [x["ms"] / args.steps for x in lv] if lv else None,
+            "last_batch_points": n_valid_last,
         }
         print(json.dumps(line), flush=True)
     if world > 1:

@@ -204,14 +204,27 @@ int vsbp_q_matrix(double f_du, double f_dv, double u0, double v0, double B, doub
  *   n_valid   : device uint64 [B], overwritten with each pair's count
  *   workspace : device scratch of compact_workspace_bytes(B, W, H) bytes
  * Points at index >= cap_points are not written (cap_points = B*W*H can never
- * overflow).  One single-pass kernel (decoupled look-back scan); async.
+ * overflow).  Count, scan and write kernels; async.
  * Errors: VSBP_EINVAL (null pointers, B < 1, W*H > 2^30, min_disp <= 0, workspace
- * too small, cap_points < 0).
+ * too small or not 256-byte aligned, cap_points < 0).
  * ------------------------------------------------------------------------- */
 size_t compact_workspace_bytes(int B, int W, int H);
 int compact_cloud_batch(int B, const float *disp, int W, int H, const double *Q, float min_disp, float *xyz,
                         long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
                         size_t ws_bytes, void *stream);
+
+/* ---------------------------------------------------------------------------
+ * jbu_compact_batch -- a6 + a7 + a8, the pipeline's call: jbu_upsample_batch
+ * (disp_hi) followed by compact_cloud_batch on its output, with the compaction's
+ * count pass folded into the JBU kernel (each valid pixel counted as it is
+ * produced) so disp_hi is read back only once.  Arguments as in those two calls;
+ * workspace of compact_workspace_bytes(B, s*W, s*H) bytes.  Results identical
+ * to the two calls made separately.
+ * ------------------------------------------------------------------------- */
+int jbu_compact_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float sigma_s,
+                      float sigma_r, int radius, const double *Q, float min_disp, float *disp_hi, float *xyz,
+                      long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
+                      size_t ws_bytes, void *stream);
 
 /* ---------------------------------------------------------------------------
  * prep_downsample_batch -- a0 (R-22): for n frames,

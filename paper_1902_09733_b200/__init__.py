@@ -94,6 +94,9 @@ _EXPORTS = {
     "compact_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "compact_cloud_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p,
                                       C.c_longlong, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "jbu_compact_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_int, C.c_float, C.c_float,
+                                    C.c_int, C.c_void_p, C.c_float, C.c_void_p, C.c_void_p, C.c_longlong, C.c_void_p,
+                                    C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
     "vsbp_strerror": (C.c_char_p, [C.c_int]),
     "vsbp_launch_count": (C.c_uint64, []),
 }
@@ -479,6 +482,39 @@ class CloudCompactor:
         return xyz, offsets, n_valid
 
 
+def jbu_compact(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_s: float, sigma_r: float, radius: int,
+                Q, min_disp: float, compactor: CloudCompactor, disp_hi: torch.Tensor | None = None,
+                xyz: torch.Tensor | None = None, offsets: torch.Tensor | None = None,
+                n_valid: torch.Tensor | None = None, stream=None):
+    """a6 + a7 + a8 (jbu_compact_batch): JBU to full res with the compaction's
+    count pass folded in, then the packed cloud.  compactor: a CloudCompactor of the
+    full-res size (its workspace is used).  Returns (disp_hi, xyz, offsets, n_valid)."""
+    if disp_lo.dim() == 2:
+        disp_lo, guide_rgb = disp_lo.unsqueeze(0), guide_rgb.unsqueeze(0)
+    B, H, W = disp_lo.shape
+    if tuple(guide_rgb.shape) != (B, H * s, W * s, 3):
+        raise ValueError("guide must be [B, s*H, s*W, 3]")
+    if (compactor.W, compactor.H) != (W * s, H * s) or B > compactor.batch:
+        raise ValueError("the compactor does not match the output size")
+    dev = disp_lo.device
+    if disp_hi is None:
+        disp_hi = torch.empty((B, H * s, W * s), dtype=torch.float32, device=dev)
+    if xyz is None:
+        xyz = torch.empty((B * H * s * W * s, 3), dtype=torch.float32, device=dev)
+    if offsets is None:
+        offsets = torch.empty(B + 1, dtype=torch.int64, device=dev)
+    if n_valid is None:
+        n_valid = torch.empty(B, dtype=torch.int64, device=dev)
+    Qh = np.ascontiguousarray(np.asarray(Q, np.float64).reshape(16))
+    _check(lib().jbu_compact_batch(B, _dev(disp_lo, torch.int32, "disp_lo"), W, H,
+                                   _dev(guide_rgb, torch.uint8, "guide_rgb"), s, sigma_s, sigma_r, radius,
+                                   Qh.ctypes.data_as(C.c_void_p), min_disp, _dev(disp_hi, torch.float32, "disp_hi"),
+                                   _dev(xyz, torch.float32, "xyz"), xyz.shape[0], _dev(offsets, torch.int64, "offsets"),
+                                   _dev(n_valid, torch.int64, "n_valid"), C.c_void_p(compactor.workspace.data_ptr()),
+                                   compactor.workspace.numel(), _stream(stream)), "jbu_compact_batch")
+    return disp_hi, xyz, offsets, n_valid
+
+
 SUMMARY_BYTES = 64
 
 
@@ -498,13 +534,25 @@ def pair_summary(disp_lo: torch.Tensor, n_valid: torch.Tensor, first_pair_id: in
 
 # ----------------------------------------------------------------------------- a0-a8
 class StereoPipeline:
-    """The whole hot path for batches of B 2.7K RGB pairs (a0-a8), all on one
-    stream: prep both frames, hierarchical BP, JBU (guide = left frame),
-    reprojection, per-pair summary.  Buffers are allocated once."""
+    """The whole hot path for batches of B virtual-stereo pairs of 2.7K RGB frames
+    (a0-a8), all on one stream: prep, hierarchical BP, JBU (guide = left frame),
+    the point cloud, per-pair summary.  Buffers are allocated once.
+
+    Two input forms:
+      * run_frames(frames [B+1,H,W,3]): B+1 consecutive frames of the video, pair j
+        = (frame j, frame j+1) -- every frame is the right view of one pair and the
+        left view of the next (S:580-583 gap = stride), so it crosses
+        the host link and is prepped ONCE;
+      * run(left [B,H,W,3], right [B,H,W,3]): independent pairs.
+    cloud="packed" (default) writes each pair's valid points in raster order
+    (compact_cloud_batch: self.xyz [cap,3], self.offsets [B+1]); cloud="dense"
+    writes the NaN-padded [B,H,W,3] cloud of the fused JBU+reprojection kernel."""
 
     def __init__(self, W_hi, H_hi, s, ndisp, levels, iters, batch, lam=0.07, data_trunc=15.0, disc_trunc=1.7,
                  sigma_s=None, sigma_r=15.0, radius=None, min_disp=1.0, Q=None, device="cuda", msg_bytes=0,
-                 camera=None, features=None, csbp_k0=None):
+                 camera=None, features=None, csbp_k0=None, cloud="packed"):
+        if cloud not in ("packed", "dense"):
+            raise ValueError("cloud must be 'packed' or 'dense'")
         self.W_hi, self.H_hi, self.s, self.B = W_hi, H_hi, s, batch
         self.W, self.H = W_hi // s, H_hi // s
         self.sigma_s = 15.0 / s if sigma_s is None else sigma_s  # R-16
@@ -512,6 +560,7 @@ class StereoPipeline:
         self.radius = -(-5 // s) if radius is None else radius
         self.min_disp = min_disp
         self.Q = Q
+        self.cloud = cloud
         if csbp_k0:
             # row f2: the constant-space BP of the paper's [4] in place of the full BP
             self.bp = ConstantSpaceBP(self.W, self.H, ndisp, levels, iters, csbp_k0, lam, data_trunc, disc_trunc,
@@ -520,12 +569,20 @@ class StereoPipeline:
             self.bp = StereoBP(self.W, self.H, ndisp, levels, iters, lam, data_trunc, disc_trunc, batch=batch,
                                msg_bytes=msg_bytes, device=device)
         dev = torch.device(device)
-        self.gray = torch.empty((2, batch, self.H, self.W), dtype=torch.uint8, device=dev)
+        # 2B grey frames: [2][B] for independent pairs, the first B+1 for a frame run
+        self.gray_flat = torch.empty((2 * batch, self.H, self.W), dtype=torch.uint8, device=dev)
+        self.gray = self.gray_flat.view(2, batch, self.H, self.W)
         self.disp = torch.empty((batch, self.H, self.W), dtype=torch.int32, device=dev)
         self.disp_hi = torch.empty((batch, H_hi, W_hi), dtype=torch.float32, device=dev)
-        self.xyz = torch.empty((batch, H_hi, W_hi, 3), dtype=torch.float32, device=dev)
         self.n_valid = torch.zeros(batch, dtype=torch.int64, device=dev)
         self.summary = torch.empty((batch, 8), dtype=torch.int64, device=dev)
+        if cloud == "packed":
+            self.compactor = CloudCompactor(W_hi, H_hi, batch, device=dev)
+            self.xyz = torch.empty((batch * H_hi * W_hi, 3), dtype=torch.float32, device=dev)
+            self.offsets = torch.zeros(batch + 1, dtype=torch.int64, device=dev)
+        else:
+            self.xyz = torch.empty((batch, H_hi, W_hi, 3), dtype=torch.float32, device=dev)
+            self.offsets = None
         # row f1: with a camera (f_u, f_v, c_u, c_v, k1, k2, k3) the raw frames are
         # undistorted first (fused with a0); the rectified left frame is the JBU guide
         self.camera = camera
@@ -533,17 +590,45 @@ class StereoPipeline:
         # left grey frame and ZSSD-matches the corners into the right one
         self.features = features
         self.corners = self.matches = None
-        self.rect = (torch.empty((batch, H_hi, W_hi, 3), dtype=torch.uint8, device=dev)
+        self.rect = (torch.empty((batch + 1, H_hi, W_hi, 3), dtype=torch.uint8, device=dev)
                      if camera is not None else None)
 
-    def run(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, first_pair_id: int = 0, stream=None):
-        """left_rgb, right_rgb: uint8 [B,H_hi,W_hi,3] on the device.  Returns the
-        per-pair summary tensor (device); disp / disp_hi / xyz stay in the object."""
-        guide = self.run_bp(left_rgb, right_rgb, stream)
-        return self.run_jbu(guide, first_pair_id, stream)
+    def cloud_of(self, pair: int) -> torch.Tensor:
+        """pair j's points of the last run: packed [n_j, 3] rows (raster order), or the
+        dense [H, W, 3] map (NaN where invalid)"""
+        if self.cloud == "dense":
+            return self.xyz[pair]
+        o = self.offsets.cpu()
+        return self.xyz[int(o[pair]):int(o[pair + 1])]
 
+    # ------------------------------------------------------------------ entry points
+    def run(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, first_pair_id: int = 0, stream=None,
+            summary_out: torch.Tensor | None = None):
+        """left_rgb, right_rgb: uint8 [B,H_hi,W_hi,3] on the device (independent pairs).
+        Returns the per-pair summary tensor (device); disp / disp_hi / xyz stay in the object."""
+        guide = self.run_bp(left_rgb, right_rgb, stream)
+        return self.run_jbu(guide, first_pair_id, stream, summary_out)
+
+    def run_frames(self, frames: torch.Tensor, first_pair_id: int = 0, stream=None,
+                   summary_out: torch.Tensor | None = None):
+        """frames: uint8 [n+1,H_hi,W_hi,3] consecutive frames on the device, n <= B:
+        the n pairs (frame j, frame j+1).  Every frame is prepped once."""
+        n = frames.shape[0] - 1
+        if n < 1 or n > self.B:
+            raise ValueError(f"need 2..{self.B + 1} frames, got {frames.shape[0]}")
+        g = self.gray_flat[:n + 1]
+        if self.camera is not None:
+            rectify_prep(frames, self.camera, self.s, gray=g, rect=self.rect[:n + 1], stream=stream)
+            guide = self.rect[:n]
+        else:
+            prep_downsample(frames, self.s, out=g, stream=stream)
+            guide = frames[:n]
+        self._bp_and_features(g[:n], g[1:n + 1], stream)
+        return self.run_jbu(guide, first_pair_id, stream, summary_out)
+
+    # ------------------------------------------------------------------ stages
     def run_bp(self, left_rgb: torch.Tensor, right_rgb: torch.Tensor, stream=None) -> torch.Tensor:
-        """a0-a5 (and f1/f3 when configured); returns the JBU guide for run_jbu."""
+        """a0-a5 (and f1/f3 when configured) for independent pairs; returns the JBU guide."""
         B = left_rgb.shape[0]
         if self.camera is not None:
             rectify_prep(left_rgb, self.camera, self.s, gray=self.gray[0, :B], rect=self.rect[:B], stream=stream)
@@ -553,71 +638,166 @@ class StereoPipeline:
             prep_downsample(left_rgb, self.s, out=self.gray[0, :B], stream=stream)
             prep_downsample(right_rgb, self.s, out=self.gray[1, :B], stream=stream)
             guide = left_rgb
-        self.bp.disparity(self.gray[0, :B], self.gray[1, :B], out=self.disp[:B], stream=stream)
-        if self.features is not None:
-            f = self.features
-            _, xy, _, _ = harris_corners(self.gray[0, :B], f.get("gc", 30), f.get("gr", 30), f.get("K", 4),
-                                         f.get("thr", 10 ** 9), stream=stream)
-            self.corners = xy
-            self.matches = zssd_match(self.gray[0, :B], self.gray[1, :B], xy, f.get("r", 5), f.get("sr", 16),
-                                      f.get("max_cost", 2 ** 62), stream=stream)
+        self._bp_and_features(self.gray[0, :B], self.gray[1, :B], stream)
         return guide
 
-    def run_jbu(self, guide: torch.Tensor, first_pair_id: int = 0, stream=None) -> torch.Tensor:
-        """a6-a8 on the labels of the last run_bp; returns the per-pair summary."""
+    def _bp_and_features(self, gl: torch.Tensor, gr: torch.Tensor, stream=None):
+        B = gl.shape[0]
+        self.bp.disparity(gl, gr, out=self.disp[:B], stream=stream)
+        if self.features is not None:
+            f = self.features
+            _, xy, _, _ = harris_corners(gl, f.get("gc", 30), f.get("gr", 30), f.get("K", 4),
+                                         f.get("thr", 10 ** 9), stream=stream)
+            self.corners = xy
+            self.matches = zssd_match(gl, gr, xy, f.get("r", 5), f.get("sr", 16), f.get("max_cost", 2 ** 62),
+                                      stream=stream)
+
+    def run_jbu(self, guide: torch.Tensor, first_pair_id: int = 0, stream=None,
+                summary_out: torch.Tensor | None = None) -> torch.Tensor:
+        """a6-a8 on the labels of the last BP; returns the per-pair summary."""
         B = guide.shape[0]
-        jbu_reproject(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
-                      self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
-                      stream=stream)
-        return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=self.summary[:B], stream=stream)
+        if self.cloud == "packed":
+            jbu_compact(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q, self.min_disp,
+                        self.compactor, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B * self.H_hi * self.W_hi],
+                        offsets=self.offsets[:B + 1], n_valid=self.n_valid[:B], stream=stream)
+        else:
+            jbu_reproject(self.disp[:B], guide, self.s, self.sigma_s, self.sigma_r, self.radius, self.Q,
+                          self.min_disp, disp_hi=self.disp_hi[:B], xyz=self.xyz[:B], n_valid=self.n_valid[:B],
+                          stream=stream)
+        out = self.summary[:B] if summary_out is None else summary_out
+        return pair_summary(self.disp[:B], self.n_valid[:B], first_pair_id, out=out, stream=stream)
+
+
+class _HostStream:
+    """Stand-in for a CUDA stream / event when the stream plumbing runs on CPU
+    tensors (tests with the gloo backend): every operation is already complete."""
+
+    def wait_event(self, ev):
+        pass
+
+    def wait_stream(self, st):
+        pass
+
+    def record(self, st=None):
+        pass
+
+    def query(self):
+        return True
+
+    def synchronize(self):
+        pass
 
 
 class StereoStream:
-    """End-to-end driver for a stream of host-resident pairs (the user-facing call):
-    pinned host RGB pairs in, per-pair summaries (and the device-resident disparity /
-    cloud of the last batch) out.  Two device input slots: the host->device copy of
-    batch i+1 runs on a copy stream while batch i computes; each batch's summary is
-    copied back to pinned host memory.  Pure stream plumbing; every step of the path
-    runs in the library's kernels (StereoPipeline)."""
+    """End-to-end driver of a video stream (the user-facing call): pinned host frame
+    batches in, per-pair summaries (and the device-resident disparity / cloud of the
+    last batch) out.
 
-    def __init__(self, pipeline: StereoPipeline, device="cuda"):
+    Batch i is B+1 consecutive frames (pairs first_pair_id + i*pair_stride + j,
+    j < B); its host->device copy runs on a copy stream while batch i-1 computes
+    (two device slots).  Each batch's summary goes to a ring of device buffers; a
+    side stream runs the optional gather (e.g. the NCCL all_gather of the
+    summaries) and the device->host copy into a ring of pinned host
+    buffers, so neither blocks the compute stream.  on_summary(i, host_tensor) is
+    called for EVERY batch, in order, as soon as its copy has landed (polled after
+    each enqueue, drained at the end).  Pure stream plumbing: every step of the
+    path runs in the library's kernels (StereoPipeline)."""
+
+    def __init__(self, pipeline, device="cuda", ring: int = 4, world: int = 1):
         self.pipe = pipeline
         dev = torch.device(device)
-        B, Hh, Wh = pipeline.B, pipeline.H_hi, pipeline.W_hi
-        self.slots = [(torch.empty((B, Hh, Wh, 3), dtype=torch.uint8, device=dev),
-                       torch.empty((B, Hh, Wh, 3), dtype=torch.uint8, device=dev)) for _ in range(2)]
-        self.copy_stream = torch.cuda.Stream(device=dev)
-        self.copied = [torch.cuda.Event() for _ in range(2)]
-        self.freed = [torch.cuda.Event() for _ in range(2)]
-        self.summary_host = torch.empty((B, 8), dtype=torch.int64).pin_memory()
         self.device = dev
+        self.cuda = dev.type == "cuda"
+        B, Hh, Wh = pipeline.B, pipeline.H_hi, pipeline.W_hi
+        self.ring, self.world = ring, world
+        self.slots = [torch.empty((B + 1, Hh, Wh, 3), dtype=torch.uint8, device=dev) for _ in range(2)]
+        self.sdev = [torch.empty((B, 8), dtype=torch.int64, device=dev) for _ in range(ring)]
+        self.gdev = [torch.empty((world * B, 8), dtype=torch.int64, device=dev) for _ in range(ring)]
+        pin = self.cuda
+        self.host = [torch.empty((world * B, 8), dtype=torch.int64, pin_memory=pin) for _ in range(ring)]
+        if self.cuda:
+            self.copy_stream = torch.cuda.Stream(device=dev)
+            self.side_stream = torch.cuda.Stream(device=dev)
+            mk = torch.cuda.Event
+        else:
+            self.copy_stream = self.side_stream = _HostStream()
+            mk = _HostStream
+        self.copied = [mk() for _ in range(2)]
+        self.freed = [mk() for _ in range(2)]
+        self.produced = [mk() for _ in range(ring)]
+        self.done = [mk() for _ in range(ring)]
+        self.h2d_bytes = self.d2h_bytes = 0
+
+    def _on(self, st):
+        import contextlib
+        return torch.cuda.stream(st) if self.cuda else contextlib.nullcontext()
+
+    def _compute(self):
+        return torch.cuda.current_stream(self.device) if self.cuda else _HostStream()
 
     def run(self, batches, first_pair_id: int = 0, gather=None, on_summary=None, pair_stride: int | None = None):
-        """batches: iterable of (left_host, right_host) pinned uint8 [B,H,W,3].
-        Enqueues everything; returns the number of batches.  gather(summary) is
-        called on the compute stream after every batch (e.g. the NCCL all_gather of
-        the summaries); on_summary(i, host tensor) after a final synchronise.
-        Batch i's pairs are numbered first_pair_id + i*pair_stride + j (pair_stride
-        defaults to B; a rank of N uses N*B, shard.batch_first_pair)."""
+        """batches: iterable of pinned host uint8 [n+1,H,W,3] frame batches, n <= B
+        (a short batch -- or None / an empty one -- ends a rank's share of the
+        stream; every rank must still pass the same number of batches when a
+        collective gather is used).  gather(summary [B,8], out [world*B,8]) runs on
+        the side stream; rows of missing pairs carry pair id -1 (shard.assemble
+        drops them).  Returns the number of batches."""
+        from collections import deque
         stride = self.pipe.B if pair_stride is None else pair_stride
-        compute = torch.cuda.current_stream(self.device)
+        compute = self._compute()
+        pending = deque()
+
+        def deliver(block: bool, most: int | None = None):
+            """hand finished batches to on_summary in order (block: wait for them)"""
+            while pending and (most is None or most > 0) and (block or pending[0][2].query()):
+                i, r, ev, rows = pending.popleft()
+                ev.synchronize()
+                if on_summary is not None:
+                    on_summary(i, self.host[r][:rows].clone())
+                if most is not None:
+                    most -= 1
+
         n = 0
-        for i, (lh, rh) in enumerate(batches):
-            k = i & 1
-            ld, rd = self.slots[k]
-            with torch.cuda.stream(self.copy_stream):
-                self.copy_stream.wait_stream(compute) if i < 2 else self.copy_stream.wait_event(self.freed[k])
-                ld.copy_(lh, non_blocking=True)
-                rd.copy_(rh, non_blocking=True)
-                self.copied[k].record(self.copy_stream)
-            compute.wait_event(self.copied[k])
-            summ = self.pipe.run(ld, rd, first_pair_id=first_pair_id + i * stride)
-            self.freed[k].record(compute)
-            if gather is not None:
-                gather(summ)
-            self.summary_host.copy_(summ, non_blocking=True)
+        B = self.pipe.B
+        for i, fh in enumerate(batches):
+            k, r = i & 1, i % self.ring
+            nf = int(fh.shape[0]) if fh is not None else 0
+            npairs = max(nf - 1, 0)  # a short (or empty) batch ends a rank's share of the stream
+            dst = self.slots[k][:nf]
+            if npairs:
+                with self._on(self.copy_stream):
+                    if i < 2:
+                        self.copy_stream.wait_stream(compute)
+                    else:
+                        self.copy_stream.wait_event(self.freed[k])
+                    dst.copy_(fh, non_blocking=True)
+                    self.copied[k].record(self.copy_stream)
+                self.h2d_bytes += fh.numel()
+            if len(pending) == self.ring:  # ring slot r is still in flight: deliver the oldest first
+                deliver(True, 1)
+            compute.wait_event(self.done[r])  # the side stream is done with sdev[r] (no-op the first time)
+            summ = self.sdev[r]
+            if npairs:
+                compute.wait_event(self.copied[k])
+                self.pipe.run_frames(dst, first_pair_id=first_pair_id + i * stride, summary_out=summ[:npairs])
+                self.freed[k].record(compute)
+            if npairs < B:
+                summ[npairs:].fill_(-1)  # padding rows (pair id -1): every rank gathers B rows
+            self.produced[r].record(compute)
+            with self._on(self.side_stream):
+                self.side_stream.wait_event(self.produced[r])
+                if gather is not None:
+                    gather(summ, self.gdev[r])
+                    src, rows = self.gdev[r], self.world * B
+                else:
+                    src, rows = summ[:npairs], npairs
+                self.host[r][:rows].copy_(src, non_blocking=True)
+                self.done[r].record(self.side_stream)
+            self.d2h_bytes += rows * 8 * 8
+            pending.append((i, r, self.done[r], rows))
+            deliver(False)
             n += 1
-        if on_summary is not None:
-            compute.synchronize()
-            on_summary(n - 1, self.summary_host)
+        deliver(True)
+        if self.cuda:
+            compute.wait_stream(self.side_stream)
         return n

@@ -70,7 +70,28 @@ struct JbuFastArgs {
     float q[16];
     float min_disp;
     int do_xyz;
+    // a8 fused counting (jbu_compact_batch): when tile_cnt != null, every pixel with
+    // D_p >= min_disp is counted into tile_cnt[b * tiles_per_pair + (raster index >> tile_shift)]
+    int *tile_cnt;
+    int tiles_per_pair, tile_shift;
 };
+
+// the valid pixels of one row segment of a warp (lane: c pixels starting at raster
+// column x of row y), counted per compaction tile; a warp's segment (<= 128 px)
+// meets at most two tiles.  Warp-uniform call.
+__device__ __forceinline__ void count_row(const JbuFastArgs &a, int b, int Wh, int y, int x, int c, bool inside)
+{
+    const int tt = inside ? (int)(((long long)y * Wh + x) >> a.tile_shift) : INT_MAX;
+    const int tA = __shfl_sync(FULL, tt, 0);
+    const int cA = __reduce_add_sync(FULL, tt == tA ? c : 0);
+    const int cB = __reduce_add_sync(FULL, (tt != tA && inside) ? c : 0);
+    const int tB = __reduce_max_sync(FULL, (tt != tA && inside) ? tt : -1);
+    if ((threadIdx.x & 31) == 0) {
+        int *base = a.tile_cnt + (size_t)b * a.tiles_per_pair;
+        if (cA) atomicAdd(base + tA, cA);
+        if (cB) atomicAdd(base + tB, cB);
+    }
+}
 
 __device__ __forceinline__ float ex2(float x)
 {
@@ -309,6 +330,7 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
         }
         disp_hi[((size_t)b * Hh + y) * Wh + x] = Dp;
     }
+    if (a.tile_cnt) count_row(a, b, Wh, y, x, (inside && Dp >= a.min_disp) ? 1 : 0, inside);
     if (!a.do_xyz) return;
     float o[3];
     const bool valid = inside && reproject_px(a, (float)x, (float)y, Dp, o);
@@ -535,6 +557,15 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
                 *reinterpret_cast<float2 *>(dst) = make_float2(Dp[r][0], Dp[r][1]);
         }
     }
+    if (a.tile_cnt) {  // a8 counts (all lanes: count_row is warp-collective)
+#pragma unroll
+        for (int r = 0; r < NR; ++r) {
+            int c = 0;
+#pragma unroll
+            for (int k = 0; k < P; ++k) c += (inside && Dp[r][k] >= a.min_disp) ? 1 : 0;
+            count_row(a, b, Wh, yb + r, x, c, inside);
+        }
+    }
     if (!a.do_xyz) continue;
     // ---- a7: 3P contiguous floats per thread and row, pixel pairs on FFMA2
 
@@ -610,7 +641,7 @@ static void launch_vec(int radius, dim3 grid, cudaStream_t st, const int32_t *di
 
 cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
                             float sigma_s, float sigma_r, int radius, const float *Qf, float min_disp, float *xyz,
-                            unsigned long long *n_valid, cudaStream_t st)
+                            unsigned long long *n_valid, cudaStream_t st, int *tile_cnt)
 {
     if (s > JB_SMAX || radius > JB_RMAX) return cudaErrorInvalidValue;
     const double log2e = 1.4426950408889634;
@@ -637,6 +668,9 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     for (int i = 0; i < 16; ++i) a.q[i] = Qf ? Qf[i] : 0.f;
     a.min_disp = min_disp;
     a.do_xyz = xyz != nullptr;
+    a.tile_cnt = tile_cnt;
+    a.tiles_per_pair = compact_tiles_per_pair(W * s, H * s);
+    a.tile_shift = __builtin_ctz((unsigned)compact_tile_pixels());
     dim3 block(JB_X, JB_Y);
     // the vector kernel needs P-aligned guide words and 4P-byte aligned outputs
     const auto al = [](const void *p, uintptr_t m) { return ((uintptr_t)p & (m - 1)) == 0; };

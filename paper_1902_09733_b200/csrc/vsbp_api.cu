@@ -610,11 +610,31 @@ int compact_cloud_batch(int B, const float *disp, int W, int H, const double *Q,
 {
     if (B < 1 || !disp || !Q || !xyz || !offsets || !n_valid || !workspace || W < 1 || H < 1) return VSBP_EINVAL;
     if ((long long)W * H > (1ll << 30) || !(min_disp > 0.f) || cap_points < 0) return VSBP_EINVAL;
-    if (ws_bytes < vsbp::compact_workspace_bytes(B, W, H) || ((uintptr_t)workspace & 7)) return VSBP_EINVAL;
+    if (ws_bytes < vsbp::compact_workspace_bytes(B, W, H) || ((uintptr_t)workspace & 255)) return VSBP_EINVAL;
     float Qf[16];
     for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
     CK(vsbp::launch_compact(B, disp, W, H, Qf, min_disp, xyz, cap_points, offsets, n_valid, workspace,
                             (cudaStream_t)stream));
+    return VSBP_OK;
+}
+
+int jbu_compact_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float sigma_s,
+                      float sigma_r, int radius, const double *Q, float min_disp, float *disp_hi, float *xyz,
+                      long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
+                      size_t ws_bytes, void *stream)
+{
+    int rc = jbu_check(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius);
+    if (rc) return rc;
+    if (!Q || !xyz || !offsets || !n_valid || !workspace || !(min_disp > 0.f) || cap_points < 0) return VSBP_EINVAL;
+    if (ws_bytes < vsbp::compact_workspace_bytes(B, W * s, H * s) || ((uintptr_t)workspace & 255)) return VSBP_EINVAL;
+    float Qf[16];
+    for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
+    cudaStream_t st = (cudaStream_t)stream;
+    CK(vsbp::compact_zero_counts(B, W * s, H * s, workspace, st));
+    CK(vsbp::launch_jbu_fast(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, nullptr, min_disp,
+                             nullptr, nullptr, st, vsbp::compact_counts(workspace)));
+    CK(vsbp::launch_compact_from_counts(B, disp_hi, W * s, H * s, Qf, min_disp, xyz, cap_points, offsets, n_valid,
+                                        workspace, st));
     return VSBP_OK;
 }
 

@@ -30,6 +30,15 @@ def batch_first_pair(step: int, rank: int, world: int, batch: int) -> int:
     return (step * world + rank) * batch
 
 
+def batch_frames(step: int, rank: int, world: int, batch: int, n_pairs: int) -> tuple[int, int]:
+    """Frames (first, count) of rank `rank`'s `step`-th batch of a video stream of
+    n_pairs pairs, pair k = (frame k, frame k+1): frames first .. first+count-1,
+    count = pairs + 1 (0 when the rank has no pair left)."""
+    first = batch_first_pair(step, rank, world, batch)
+    pairs = max(0, min(batch, n_pairs - first))
+    return first, pairs + 1 if pairs else 0
+
+
 def rank_of_pair(pair: int, world: int, batch: int) -> int:
     return (pair // batch) % world
 

@@ -677,30 +677,81 @@ def test_icp_failure_and_identity():
 
 # ----------------------------------------------------------------------------- bench configuration
 def test_bench_launch_configuration_sampled_pairs():
-    """The configuration bench.py times (C5: 128 pairs per launch -- bench.py's
-    default batch --, 2.7K RGB, s=4, L=64, 5x5, JBU r=2): three sampled pairs of the
-    batch (first, middle, last; two different scenes) through the whole path against
-    the oracle."""
+    """The configuration bench.py times (C5: one batch of 128 pairs = 129 consecutive
+    frames of the synthetic 2.7K video, s=4, L=64, 5x5, JBU r=2, packed clouds):
+    three sampled pairs of a batch deep into the stream (first, middle, last) through
+    the whole path against the oracle -- disparities bit-exact, JBU within 1e-4 px,
+    the packed cloud's counts exact and its points within 1e-5 relative."""
     import bench
+    from synthgen import video
     B = 128
     I = synthgen.INTRINSICS
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(bench.W_HI, bench.H_HI, bench.S_DOWN, bench.NDISP, bench.LEVELS, bench.ITERS, batch=B,
                             Q=Q, device=dev())
-    lp, rp = bench.make_pool(7000, 2)
-    idx = [0] * B
-    idx[B // 2] = idx[B - 1] = 1
-    sel = torch.tensor(idx, device=dev())
-    summ = pipe.run(to_dev(lp)[sel].contiguous(), to_dev(rp)[sel].contiguous(), first_pair_id=5).cpu().numpy()
+    frames = torch.empty((B + 1, bench.H_HI, bench.W_HI, 3), dtype=torch.uint8, device=dev())
+    video.frames_device(bench.video_scene(1902), 17 * B, frames)
+    summ = pipe.run_frames(frames, first_pair_id=17 * B).cpu().numpy()
+    off = pipe.offsets.cpu().numpy()
     Qo = oracle.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     for b in (0, B // 2, B - 1):
-        k = idx[b]
-        disp_o, hi_o, _, n_o = oracle.pipeline_pair(lp[k], rp[k], bench.S_DOWN, bench.NDISP, bench.LEVELS,
-                                                    bench.ITERS, Qo)
+        l, r = frames[b].cpu().numpy(), frames[b + 1].cpu().numpy()
+        disp_o, hi_o, _, n_o = oracle.pipeline_pair(l, r, bench.S_DOWN, bench.NDISP, bench.LEVELS, bench.ITERS, Qo)
         assert np.array_equal(pipe.disp[b].cpu().numpy(), disp_o)
-        assert np.max(np.abs(pipe.disp_hi[b].cpu().numpy().astype(np.float64) - hi_o)) <= 1e-4
+        hi_g = pipe.disp_hi[b].cpu().numpy().astype(np.float64)
+        assert np.max(np.abs(hi_g - hi_o)) <= 1e-4
         amb = int(np.sum(np.abs(hi_o - 1.0) < 1e-4))
-        assert abs(int(summ[b, 0]) - n_o) <= amb and int(summ[b, 3]) == 5 + b
+        assert abs(int(summ[b, 0]) - n_o) <= amb and int(summ[b, 3]) == 17 * B + b
+        ref = oracle.compact_cloud(hi_g, Qo, 1.0)  # the GPU's own f32 disparities: exact count
+        assert off[b + 1] - off[b] == ref.shape[0] == int(summ[b, 0])
+        got = pipe.xyz[off[b]:off[b + 1]].cpu().numpy().astype(np.float64)
+        err = np.linalg.norm(got - ref, axis=1) / np.linalg.norm(ref, axis=1)
+        assert err.max() <= 1e-5
+
+
+def test_frames_run_equals_independent_pairs():
+    """run_frames on n+1 consecutive frames (each frame prepped once) gives exactly
+    what run() gives on the n pairs (frame j, frame j+1) passed separately."""
+    from synthgen import video
+    W, H, n = 512, 256, 5
+    sc = video.VideoScene(77, W, H, 4, 8, 48)
+    frames = torch.empty((n + 1, H, W, 3), dtype=torch.uint8, device=dev())
+    video.frames_device(sc, 40, frames)
+    Q = P.q_matrix(700.0, 700.0, W / 2 - 0.5, H / 2 - 0.5, 0.5)
+    a = P.StereoPipeline(W, H, 4, 64, 4, 5, batch=n, Q=Q, device=dev())
+    b = P.StereoPipeline(W, H, 4, 64, 4, 5, batch=n, Q=Q, device=dev())
+    sa = a.run_frames(frames, first_pair_id=9)
+    sb = b.run(frames[:n].contiguous(), frames[1:].contiguous(), first_pair_id=9)
+    assert torch.equal(sa, sb) and torch.equal(a.disp, b.disp) and torch.equal(a.disp_hi, b.disp_hi)
+    assert torch.equal(a.offsets, b.offsets)
+    assert torch.equal(a.xyz[: int(a.offsets[-1])], b.xyz[: int(b.offsets[-1])])
+    ld = oracle.prep(frames[2].cpu().numpy(), 4)
+    assert np.array_equal(a.gray_flat[2].cpu().numpy(), ld)
+
+
+def test_stream_driver_on_gpu_every_batch():
+    """StereoStream end to end on the device (pinned host frame batches, copy stream,
+    side-stream D2H ring smaller than the batch count): every batch's summaries reach
+    on_summary in order and equal a direct run_frames of the same frames; a short
+    last batch is handled."""
+    from synthgen import video
+    W, H, B = 256, 128, 3
+    sc = video.VideoScene(5, W, H, 4, 8, 48)
+    frames = torch.empty((3 * B + 1, H, W, 3), dtype=torch.uint8, device=dev())
+    video.frames_device(sc, 0, frames)
+    host = frames.cpu().pin_memory()
+    batches = [host[0:B + 1], host[B:2 * B + 1], host[2 * B:3 * B], host[0:B + 1]]  # third is short
+    Q = P.q_matrix(700.0, 700.0, W / 2 - 0.5, H / 2 - 0.5, 0.5)
+    pipe = P.StereoPipeline(W, H, 4, 16, 2, 5, batch=B, Q=Q, device=dev())
+    got = []
+    P.StereoStream(pipe, device=dev(), ring=2).run(batches, first_pair_id=100, on_summary=lambda i, t: got.append((i, t)))
+    torch.cuda.synchronize()
+    assert [i for i, _ in got] == [0, 1, 2, 3]
+    ref = P.StereoPipeline(W, H, 4, 16, 2, 5, batch=B, Q=Q, device=dev())
+    for i, t in got:
+        want = ref.run_frames(batches[i].to(dev()), first_pair_id=100 + i * B).cpu()
+        assert torch.equal(t, want[: t.shape[0]]), i
+    assert got[2][1].shape[0] == B - 1
 
 
 def test_config4_pipeline_jbu_s2_r3():
@@ -830,3 +881,24 @@ def test_compact_cloud_full_frames_sampled():
         got = xyz[off.cpu().numpy()[b] + idx]
         err = np.linalg.norm(got - ref[idx], axis=1) / np.linalg.norm(ref[idx], axis=1)
         assert err.max() <= 1e-5
+
+
+@pytest.mark.parametrize("s,r,W,H,B", [(4, 2, 173, 61, 3), (2, 3, 130, 47, 2), (3, 2, 41, 29, 2), (8, 1, 40, 20, 2),
+                                       (4, 5, 676, 380, 1)])
+def test_jbu_compact_equals_separate_calls(s, r, W, H, B):
+    """jbu_compact_batch (counts folded into the JBU kernel, vector and scalar
+    kernels) == jbu_upsample_batch + compact_cloud_batch, bit for bit, including
+    pairs with invalid regions and tiles that straddle rows."""
+    rng = np.random.default_rng(s * W + r)
+    lo = rng.integers(0, 40, size=(B, H, W)).astype(np.int32)
+    lo[0, : H // 3] = 0  # a band of invalid (d < min_disp) pixels
+    guide = np.stack([synthgen.value_noise_rgb(b + s, W * s, H * s) for b in range(B)])
+    Q = P.q_matrix(900.0, 880.0, W * s / 2, H * s / 2, 0.5)
+    comp = P.CloudCompactor(W * s, H * s, B, device=dev())
+    hi, xyz, off, nv = P.jbu_compact(to_dev(lo), to_dev(guide), s, 2.5, 20.0, r, Q, 1.0, comp)
+    hi2 = P.jbu_upsample(to_dev(lo), to_dev(guide), s, 2.5, 20.0, r)
+    xyz2, off2, nv2 = P.CloudCompactor(W * s, H * s, B, device=dev())(hi2, Q, 1.0)
+    torch.cuda.synchronize()
+    assert torch.equal(hi, hi2) and torch.equal(off, off2) and torch.equal(nv, nv2)
+    assert torch.equal(xyz[: int(off[-1])], xyz2[: int(off2[-1])])
+    assert int(off[-1]) == int((hi2 >= 1.0).sum())

@@ -89,3 +89,85 @@ def test_world2_gloo_gather_matches_serial():
         full = torch.load(out)
     serial = torch.tensor([_pair_summary_row(p) for p in range(N_PAIRS)], dtype=torch.int64)
     assert torch.equal(full, serial)
+
+
+# ----------------------------------------------------------------------------- the stream driver on 2 ranks
+S_PAIRS, S_BATCH, S_H, S_W = 17, 3, 2, 5
+
+
+def _frame(k: int) -> torch.Tensor:
+    """a tiny frame whose first two bytes encode its index in the video"""
+    f = torch.zeros((S_H, S_W, 3), dtype=torch.uint8)
+    f[0, 0, 0], f[0, 0, 1] = k % 256, k // 256
+    return f
+
+
+class _FramePipe:
+    """CPU stand-in for StereoPipeline.run_frames: the summary row of pair j records
+    which frames it was given (left, right) and its pair id -- the host logic of
+    StereoStream (frame routing, pair numbering, ring, gather, delivery) is what is
+    under test, not the method's arithmetic."""
+
+    def __init__(self):
+        self.B, self.H_hi, self.W_hi = S_BATCH, S_H, S_W
+
+    def run_frames(self, frames, first_pair_id=0, stream=None, summary_out=None):
+        ids = frames[:, 0, 0, 0].to(torch.int64) + 256 * frames[:, 0, 0, 1].to(torch.int64)
+        n = frames.shape[0] - 1
+        summary_out.zero_()
+        summary_out[:, 0] = ids[:n]
+        summary_out[:, 1] = ids[1:n + 1]
+        summary_out[:, shard.PAIR_ID] = first_pair_id + torch.arange(n)
+        return summary_out
+
+
+def _stream_worker(rank: int, port: int, out_path: str):
+    import paper_1902_09733_b200 as P
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=WORLD)
+    try:
+        runner = P.StereoStream(_FramePipe(), device="cpu", ring=2, world=WORLD)
+        batches = []
+        for step in range(shard.steps_for(S_PAIRS, WORLD, S_BATCH)):
+            first, count = shard.batch_frames(step, rank, WORLD, S_BATCH, S_PAIRS)
+            batches.append(torch.stack([_frame(first + i) for i in range(count)]) if count else None)
+        got = []
+        n = runner.run(batches, first_pair_id=shard.batch_first_pair(0, rank, WORLD, S_BATCH),
+                       pair_stride=WORLD * S_BATCH,
+                       gather=lambda summ, out: shard.gather_summaries(summ, out=out),
+                       on_summary=lambda i, t: got.append((i, t)))
+        assert n == len(batches) and [i for i, _ in got] == list(range(n)), "every batch delivered, in order"
+        if rank == 0:
+            full = shard.assemble(torch.cat([t for _, t in got]), n_pairs=S_PAIRS)
+            torch.save(full, out_path)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_world2_stream_driver_routes_frames_and_numbers_pairs():
+    """StereoStream.run(gather=..., pair_stride=world*B) on two
+    gloo ranks over a shared-frame stream of 17 pairs in batches of 3 (the last batch
+    of one rank short, the other rank's last step empty): after the all_gather and
+    shard.assemble every pair p appears once, built from frames (p, p+1)."""
+    port = _free_port()
+    with tempfile.TemporaryDirectory() as d:
+        out = os.path.join(d, "stream.pt")
+        mp.spawn(_stream_worker, args=(port, out), nprocs=WORLD, join=True)
+        full = torch.load(out)
+    p = torch.arange(S_PAIRS)
+    assert torch.equal(full[:, shard.PAIR_ID], p)
+    assert torch.equal(full[:, 0], p) and torch.equal(full[:, 1], p + 1)
+
+
+def test_stream_driver_single_process_delivers_every_batch():
+    """every batch's summaries reach on_summary (ring smaller than the
+    number of batches), with no gather."""
+    import paper_1902_09733_b200 as P
+    runner = P.StereoStream(_FramePipe(), device="cpu", ring=2, world=1)
+    batches = [torch.stack([_frame(3 * i + j) for j in range(4)]) for i in range(5)]
+    got = []
+    runner.run(batches, on_summary=lambda i, t: got.append((i, t)))
+    assert [i for i, _ in got] == list(range(5))
+    for i, t in got:
+        assert t[:, shard.PAIR_ID].tolist() == [3 * i + j for j in range(3)]
+        assert t[:, 0].tolist() == [3 * i + j for j in range(3)] and t[:, 1].tolist() == [3 * i + j + 1 for j in range(3)]
