@@ -51,6 +51,12 @@
 
 namespace vsbp {
 
+// VSBP_JBU_UNROLL_TY: unroll the window's rows in the vector kernel (1: the whole
+// (2R+1)^2 x 8-pixel body is straight-line code; 0: one row per loop trip, a 5x
+// smaller hot loop for the instruction cache)
+#ifndef VSBP_JBU_UNROLL_TY
+#define VSBP_JBU_UNROLL_TY 1
+#endif
 // JB_RP: row passes per CTA of the vector kernel (one staged footprint serves
 // JB_RP x JB_Y rows; fewer redundantly staged halo rows per pixel)
 #ifndef JB_RP
@@ -402,12 +408,12 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     static_assert(S % P == 0, "a thread's P pixels must share one footprint");
     // NR rows per thread: rows 2t, 2t+1 of a tile are in one footprint row pair (S even)
     constexpr int NT = JB_X * JB_Y / NR;
-    __shared__ uint2 sT[JB_LW * JB_LH];
+    // the staged footprint of the CTA's JB_X P x JB_Y JB_RP pixels (sized
+    // from JB_RP, R and S, not from the scalar kernel's array)
+    constexpr int VLW = (JB_X * P) / S + 2 * R + 1, VLH = (JB_Y * JB_RP + S - 1) / S + 2 * R + 1;
+    __shared__ uint2 sT[VLW * VLH];
     __shared__ unsigned warp_cnt[NT / 32];
     __shared__ int wlo[NT / 32], whi[NT / 32];
-    // the staged footprint (JB_X P / S + 2R + 1) x (JB_Y JB_RP / S + 2R + 1) fits sT
-    static_assert((JB_X * P) / S + 2 * R + 1 <= JB_LW && (JB_Y * JB_RP + S - 1) / S + 2 * R + 1 <= JB_LH,
-                  "JB_RP / R too large for the staged tap array");
     const int b = blockIdx.z;
     const int Wh = a.W * S, Hh = a.H * S;
     const int x0 = blockIdx.x * (JB_X * P), y0 = blockIdx.y * (JB_Y * JB_RP);
@@ -420,6 +426,28 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     const bool wide = tile_wide(wlo, whi, NT / 32, a);
     const int x = x0 + P * threadIdx.x;
     int cnt = 0;
+    // per-thread constants of every row pass: the column's x spatial exponents (with
+    // out-of-image columns at -inf) and the row sub-position's y factors (JB_Y is a
+    // multiple of S, so v0 is the same in every pass)
+    const int cx = x / S;
+    const int u0 = S == P ? 0 : x - cx * S;
+    const int v0 = (y0 + NR * threadIdx.y) % S;
+    f2_t sx2[P / 2][T];
+#if VSBP_JBU_UNROLL_TY
+    float ryv[NR][T];
+#endif
+#pragma unroll
+    for (int t = 0; t < T; ++t) {
+        const int qx = cx - R + t;
+        const bool okx = qx >= 0 && qx < a.W;
+#pragma unroll
+        for (int j = 0; j < P / 2; ++j)
+            sx2[j][t] = okx ? pk2(a.sxt[u0 + 2 * j][t], a.sxt[u0 + 2 * j + 1][t]) : pk2(-INFINITY, -INFINITY);
+#if VSBP_JBU_UNROLL_TY
+#pragma unroll
+        for (int r = 0; r < NR; ++r) ryv[r][t] = a.ryt[v0 + r][t];
+#endif
+    }
 #pragma unroll 1
     for (int rp = 0; rp < JB_RP; ++rp) {
     const int yb = y0 + rp * JB_Y + NR * threadIdx.y;
@@ -433,21 +461,17 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         unsigned Ip[NR][P];
 #pragma unroll
         for (int r = 0; r < NR; ++r) GuideVec<P>::load(G + ((size_t)(yb + r) * Wh + x) * 3, Ip[r]);
-        const int cx = x / S, cy = yb / S;
-        const int u0 = S == P ? 0 : x - cx * S;
-        const int v0 = yb - cy * S;
+        const int cy = yb / S;
+#if VSBP_JBU_UNROLL_TY
         float rfl[NR][T];
-        f2_t sx2[P / 2][T];
 #pragma unroll
         for (int t = 0; t < T; ++t) {
-            const int qy = cy - R + t, qx = cx - R + t;
-            const bool oky = qy >= 0 && qy < a.H, okx = qx >= 0 && qx < a.W;
+            const int qy = cy - R + t;
+            const bool oky = qy >= 0 && qy < a.H;
 #pragma unroll
-            for (int r = 0; r < NR; ++r) rfl[r][t] = oky ? a.ryt[v0 + r][t] : 0.f;
-#pragma unroll
-            for (int j = 0; j < P / 2; ++j)
-                sx2[j][t] = okx ? pk2(a.sxt[u0 + 2 * j][t], a.sxt[u0 + 2 * j + 1][t]) : pk2(-INFINITY, -INFINITY);
+            for (int r = 0; r < NR; ++r) rfl[r][t] = oky ? ryv[r][t] : 0.f;
         }
+#endif
         const int e0 = (cy - R - ly0) * lw + (cx - R - lx0);
         const unsigned cen = sT[e0 + R * lw + R].x;
         const float cf = __uint_as_float(sT[e0 + R * lw + R].y);
@@ -476,7 +500,7 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
                     if (ref[r][k] <= a.far_thr) continue;
 #pragma unroll
                     for (int ty = 0; ty < T; ++ty) {
-                        if (rfl[r][ty] == 0.f) continue;
+                        if (cy - R + ty < 0 || cy - R + ty >= a.H) continue;
                         for (int tx = 0; tx < T; ++tx) {
                             const int qx = cx - R + tx;
                             if (qx < 0 || qx >= a.W) continue;
@@ -498,7 +522,11 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         for (int r = 0; r < NR; ++r)
 #pragma unroll
             for (int j = 0; j < P / 2; ++j) num[r][j] = den[r][j] = 0ull;
+#if VSBP_JBU_UNROLL_TY
 #pragma unroll
+#else
+#pragma unroll 1
+#endif
         for (int ty = 0; ty < T; ++ty) {
             f2_t nr[NR][P / 2], dr[NR][P / 2];
 #pragma unroll
@@ -528,7 +556,13 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
             }
 #pragma unroll
             for (int r = 0; r < NR; ++r) {
+#if VSBP_JBU_UNROLL_TY
                 const f2_t rf2 = pk2(rfl[r][ty], rfl[r][ty]);
+#else
+                const int qy = cy - R + ty;
+                const float rf = (qy >= 0 && qy < a.H) ? a.ryt[v0 + r][ty] : 0.f;
+                const f2_t rf2 = pk2(rf, rf);
+#endif
 #pragma unroll
                 for (int j = 0; j < P / 2; ++j) {
                     num[r][j] = fma2(rf2, nr[r][j], num[r][j]);
