@@ -298,7 +298,10 @@ __global__ void __launch_bounds__(128) k_csbp_init_par(const uint8_t *__restrict
 }
 
 // k_csbp_update_par: one thread per (sender pixel, receiver candidate j); GP = pow2 >= k
-// lanes per pixel; the sender's h is rebuilt per lane from L1-resident rows.
+// lanes per pixel (up to 64: the minimum over two warps goes through shared memory);
+// the sender's h is rebuilt per lane from L1-resident rows.  The serial k_csbp_update
+// (one thread per pixel, O(k^2) in a thread) was 368 us per launch on C4's 43 x 24
+// top level at k = 64 (ncu, r02): too few threads.
 __global__ void __launch_bounds__(128) k_csbp_update_par(CsbpArgs a, CsbpLevel lv, int colour, int GP)
 {
     const int b = blockIdx.y;
@@ -338,7 +341,14 @@ __global__ void __launch_bounds__(128) k_csbp_update_par(CsbpArgs a, CsbpLevel l
             m = min(best, hmin + a.tau_q);
         }
         int mmin = m;
-        for (int o = GP >> 1; o > 0; o >>= 1) mmin = min(mmin, __shfl_xor_sync(0xffffffffu, mmin, o, GP));
+        for (int o = min(GP, 32) >> 1; o > 0; o >>= 1) mmin = min(mmin, __shfl_xor_sync(0xffffffffu, mmin, o, min(GP, 32)));
+        if (GP > 32) {  // GP = 64: the pixel's two warps combine their minima (block-uniform branch)
+            __shared__ int wmin[4];
+            if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mmin;
+            __syncthreads();
+            mmin = min(wmin[threadIdx.x >> 5], wmin[(threadIdx.x >> 5) ^ 1]);
+            __syncthreads();
+        }
         if (go) {
             const size_t q = (size_t)b * lv.n + (size_t)(y + dys[kk]) * lv.W + (x + dxs[kk]);
             lv.msg[q * 4 * k + (size_t)opp[kk] * k + lane] = m - mmin;
@@ -390,7 +400,7 @@ cudaError_t launch_csbp_update(const CsbpArgs &a, const CsbpLevel &lv, int colou
 {
     if (lv.k > CS_KMAX) return cudaErrorInvalidValue;
     const int nc = ((lv.W + 1) >> 1) * lv.H;
-    if (lv.k >= 8 && lv.k <= 32) {  // one warp-segment per pixel (shuffle width <= 32)
+    if (lv.k >= 8) {  // GP = pow2 >= k lanes per pixel (k = 33..64: two warps per pixel)
         int GP = 1;
         while (GP < lv.k) GP <<= 1;
         const int ppb = 128 / GP;

@@ -12,6 +12,8 @@
 #include "vsbp_internal.cuh"
 #include "vsbp_kernels.h"
 
+constexpr int EV_RING = 1024;  // pending level timings (bp_timing_enable)
+
 struct vsbp_bp {
     int W, H, L, levels, iters;
     int lam_q, tau_d, tau_q, S;
@@ -30,12 +32,14 @@ struct vsbp_bp {
     int last_B;
     const uint8_t *last_left, *last_right;  // the last call's images (debug cost export)
     // live timing of the a4 launches (bp_timing_enable)
+    // a FIFO ring of EV_RING (start, end) event pairs, one per level per call,
+    // drained without blocking as the events complete
     int timing;
-    int n_pending;
-    cudaEvent_t ev[64][2];
-    int ev_level[64];
-    int ev_launches[64];
-    double ev_bytes[64];
+    int ev_head, n_pending;
+    cudaEvent_t ev[EV_RING][2];
+    int ev_level[EV_RING];
+    int ev_launches[EV_RING];
+    double ev_bytes[EV_RING];
     double acc_ms[16], acc_bytes[16];
     int64_t acc_launches[16];
 };
@@ -175,18 +179,29 @@ namespace vsbp {
 void note_launch(int n) { g_launches += (uint64_t)n; }
 }  // namespace vsbp
 
-static int timing_drain(vsbp_bp *c)
+// Accumulate the pending level timings in FIFO order.  block = 0: only those whose
+// end event has already completed (cudaEventQuery; never waits on the device);
+// block = 1: all of them (bp_timing_read).
+static int timing_drain(vsbp_bp *c, int block)
 {
-    for (int i = 0; i < c->n_pending; ++i) {
+    while (c->n_pending > 0) {
+        const int i = c->ev_head;
+        if (!block) {
+            const cudaError_t q = cudaEventQuery(c->ev[i][1]);
+            if (q == cudaErrorNotReady) break;
+            CK(q);
+        } else {
+            CK(cudaEventSynchronize(c->ev[i][1]));
+        }
         float ms = 0.f;
-        CK(cudaEventSynchronize(c->ev[i][1]));
         CK(cudaEventElapsedTime(&ms, c->ev[i][0], c->ev[i][1]));
         const int l = c->ev_level[i];
         c->acc_ms[l] += ms;
         c->acc_launches[l] += c->ev_launches[i];
         c->acc_bytes[l] += c->ev_bytes[i];
+        c->ev_head = (c->ev_head + 1) % EV_RING;
+        --c->n_pending;
     }
-    c->n_pending = 0;
     return VSBP_OK;
 }
 
@@ -334,8 +349,10 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
     if (!c || !left || !right || !disp || B < 1) return VSBP_EINVAL;
     if (!c->ws || B > c->ws_batch) return VSBP_EDIM;
     cudaStream_t st = (cudaStream_t)stream;
-    if (c->timing && c->n_pending + c->levels > 64) {
-        int rc = timing_drain(c);
+    if (c->timing) {
+        int rc = timing_drain(c, 0);
+        // a full ring (thousands of calls without a read) is the one case that waits
+        if (!rc && c->n_pending + c->levels > EV_RING) rc = timing_drain(c, 1);
         if (rc) return rc;
     }
     // the workspace is planned for ws_batch pairs: level arrays are [ws_batch][...],
@@ -398,7 +415,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 CK(vsbp::launch_upcopy(M, Mp, c->msg_bytes, g, 1, st));
             }
         }
-        const int slot = (c->timing && c->n_pending < 64) ? c->n_pending++ : -1;
+        const int slot = c->timing ? (c->ev_head + c->n_pending++) % EV_RING : -1;
         if (slot >= 0) CK(cudaEventRecord(c->ev[slot][0], st));
         double bytes = 0.0;
         const bool fast = use_fast(c, l);
@@ -437,7 +454,17 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
             // pixels of colour t&1: ceil/floor split of each row
             long long npix = 0;
             for (int y = 0; y < g.H; ++y) npix += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;
-            bytes += (double)B * npix * ((double)c->L * c->dbytes[l] + 8.0 * c->L * c->msg_bytes);
+            if (mode == 2) {
+                // first iteration below the top (a3 virtual up-copy): D and the 4 outgoing
+                // messages per updated pixel, plus the parent level's message planes read
+                // once (4 L bytes per parent pixel; its children read them from L2) --
+                // not 4 incoming per child (that undercounts ncu's DRAM by 23 %)
+                const vsbp::Geom gp = geom(c, B, l + 1);
+                bytes += (double)B * (npix * ((double)c->L * c->dbytes[l] + 4.0 * c->L * c->msg_bytes) +
+                                      (double)gp.W * gp.H * 4.0 * c->L * c->msg_bytes);
+            } else {
+                bytes += (double)B * npix * ((double)c->L * c->dbytes[l] + 8.0 * c->L * c->msg_bytes);
+            }
         }
         if (slot >= 0) {
             CK(cudaEventRecord(c->ev[slot][1], st));
@@ -509,13 +536,14 @@ int bp_timing_enable(vsbp_bp *c, int enable)
 {
     if (!c) return VSBP_EINVAL;
     if (enable && !c->timing) {
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < EV_RING; ++i)
             for (int j = 0; j < 2; ++j) CK(cudaEventCreate(&c->ev[i][j]));
+        c->ev_head = c->n_pending = 0;
     }
     if (!enable && c->timing) {
-        for (int i = 0; i < 64; ++i)
+        for (int i = 0; i < EV_RING; ++i)
             for (int j = 0; j < 2; ++j) cudaEventDestroy(c->ev[i][j]);
-        c->n_pending = 0;
+        c->ev_head = c->n_pending = 0;
     }
     c->timing = enable ? 1 : 0;
     return VSBP_OK;
@@ -525,7 +553,7 @@ int bp_timing_read(vsbp_bp *c, double *ms, int64_t *launches, double *bytes)
 {
     if (!c || !ms || !launches || !bytes) return VSBP_EINVAL;
     if (!c->timing) return VSBP_EINVAL;
-    int rc = timing_drain(c);
+    int rc = timing_drain(c, 1);
     if (rc) return rc;
     for (int l = 0; l < 16; ++l) {
         ms[l] = c->acc_ms[l];

@@ -609,6 +609,16 @@ def test_csbp_fuzz(seed):
     check_csbp(left, right, L, levels, iters, k0)
 
 
+@pytest.mark.parametrize("W,H,L,levels,k0", [(37, 23, 64, 3, 16), (29, 17, 48, 2, 24), (45, 9, 64, 2, 33)])
+def test_csbp_wide_candidate_sets(W, H, L, levels, k0):
+    """k_l between 33 and 64 (two warps per pixel in the parallel update, C4's top
+    level at k0 = 2 has k = 64)."""
+    rng = np.random.default_rng(W * L + k0)
+    left = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    right = rng.integers(0, 256, size=(H, W), dtype=np.uint8)
+    check_csbp(left, right, L, levels, 4, k0)
+
+
 def test_csbp_config2_full_size():
     """676x380, L=64, 5 levels x 5 iterations, k0=2 (k = 2,4,8,16,32)."""
     left, right, d_lo = synthgen.stereo_pair_rgb(0)

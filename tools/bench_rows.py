@@ -80,6 +80,13 @@ def main():
     res["c4_bp_1352x760_L128_6x8"] = {"ms_per_pair": ms_bp4, "pairs_per_s": 1e3 / ms_bp4,
                                        "workspace_MB_per_pair": bp4.workspace.numel() / B4 / 1e6}
     res["c4_jbu_s2_r3_reproject"] = {"ms_per_pair": ms_jbu4}
+    # f2 at C4, where constant-space BP should pay (12.6 GB/pair of full-BP message
+    # traffic at u16; k_l = min(128, k0 2^l) <= 64 candidates -> k0 <= 2)
+    for k0 in (1, 2):
+        cs4 = P.ConstantSpaceBP(1352, 760, 128, 6, 8, k0, batch=B4, device=dev)
+        res[f"f2_csbp_c4_k0_{k0}"] = {"ms_per_pair": timed(lambda: cs4.disparity(gl2, gr2, out=out4), reps=5) / B4,
+                                      "workspace_MB_per_pair": cs4.workspace.numel() / B4 / 1e6}
+        del cs4
     del bp4, out4, o4
     for k0 in (1, 2, 4):
         cs = P.ConstantSpaceBP(676, 380, 64, 5, 5, k0, batch=B, device=dev)
