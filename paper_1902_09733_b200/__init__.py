@@ -32,6 +32,8 @@ VSBP_OPT_MSG_BYTES = 1
 VSBP_OPT_KERNEL = 2
 VSBP_OPT_DIMG = 3
 VSBP_OPT_FINAL = 4
+VSBP_OPT_PAIR = 5
+VSBP_OPT_PAIR_BAND = 6
 _ERRNAMES = {-1: "VSBP_EINVAL", -2: "VSBP_EDIM", -3: "VSBP_EOVERFLOW", -4: "VSBP_ECUDA"}
 
 
@@ -148,7 +150,7 @@ class StereoBP:
     device workspace (a torch uint8 tensor) for up to ``batch`` pairs."""
 
     def __init__(self, W, H, ndisp, levels, iters, lam=0.07, data_trunc=15.0, disc_trunc=1.7, batch=1,
-                 msg_bytes=0, kernel=0, device="cuda", dimg=0, final=None):
+                 msg_bytes=0, kernel=0, device="cuda", dimg=0, final=None, pair=None, pair_band=None):
         self._h = C.c_void_p()
         _check(lib().bp_create(W, H, ndisp, levels, iters, lam, data_trunc, disc_trunc, C.byref(self._h)),
                "bp_create")
@@ -162,6 +164,13 @@ class StereoBP:
             final = int(os.environ.get("VSBP_FINAL", "0"))
         if final:  # fused last level-0 iteration + WTA (level-0 messages not stored)
             _check(lib().bp_set_option(self._h, VSBP_OPT_FINAL, final), "bp_set_option")
+        if pair is None:  # experiment knob: VSBP_PAIR=0 disables two iterations per launch
+            pair = int(os.environ.get("VSBP_PAIR", "1"))
+        _check(lib().bp_set_option(self._h, VSBP_OPT_PAIR, int(pair)), "bp_set_option")
+        if pair_band is None and os.environ.get("VSBP_PAIR_BAND"):
+            pair_band = int(os.environ["VSBP_PAIR_BAND"])
+        if pair_band:
+            _check(lib().bp_set_option(self._h, VSBP_OPT_PAIR_BAND, int(pair_band)), "bp_set_option")
         self.W, self.H, self.L, self.levels, self.iters, self.batch = W, H, ndisp, levels, iters, batch
         nbytes = int(lib().bp_workspace_bytes(self._h, batch))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)

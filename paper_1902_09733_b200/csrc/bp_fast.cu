@@ -640,6 +640,311 @@ cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn,
     return cudaGetLastError();
 }
 
+// ---------------------------------------------------------------- two iterations per launch
+// k_update_pair: checkerboard iterations t (colour A = a.colour) and t+1 (colour B)
+// in one launch (north_star "several checkerboard iterations per launch";
+// DESIGN §8).  The messages colour A sends at iteration t are read by exactly one
+// consumer -- colour B's update at t+1 -- and are rewritten at t+2 before anything
+// else reads them, so they never go to HBM: a CTA walks down the rows of a band of
+// its column tile, and for every row ya
+//   A-phase: updates the colour-A pixels of row ya (plus one halo pixel on each
+//            side of the tile) from colour B's iteration-(t-1) messages (or from the
+//            parent level, MODE 2; or from nothing, MODE 1) and keeps their four
+//            outgoing messages in a 3-row shared-memory ring;
+//   B-phase: updates the colour-B pixels of row ya-1 from the ring (rows ya-2,
+//            ya-1, ya) and writes their messages to the level's OTHER message array
+//            (a.Mw): colour-B messages of iteration t-1 are still being read by the
+//            neighbouring tiles and bands, so the level's messages ping-pong between
+//            two arrays at every fused pair (the host switches its base pointer).
+// Per pixel pair HBM carries D_A + D_B + colour-B messages in (4L) and out (4L) --
+// 10L bytes at u8 -- instead of 2 x 9L for two single-iteration launches.  The
+// arithmetic per pixel is k_update_fast's, so the messages are bit-identical.
+// The colour-A halo (2 pixels per 64-pixel tile row, 2 rows per band) is computed
+// twice.  Requires TD = u8 / u16 D, u8 messages (the fast-kernel domain).
+template <bool PAD, bool SIGNED, typename Store>
+__device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8], const uint32_t (&in)[4][8],
+                                         const uint32_t padm[8], int lane_g, Store store)
+{
+#pragma unroll
+    for (int kp = 0; kp < 4; kp += 2) {
+        uint32_t h[2][8];
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+            const uint32_t base = kp == 0 ? iadd3(dv[j], in[2][j], in[3][j]) : iadd3(dv[j], in[0][j], in[1][j]);
+            h[0][j] = base + in[kp + 1][j];
+            h[1][j] = base + in[kp][j];
+            if (PAD) {
+                h[0][j] |= padm[j];
+                h[1][j] |= padm[j];
+            }
+        }
+        uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
+        for (int s = a.G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, a.G));
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
+            if (SIGNED) {
+                const uint32_t neg = prmt(0u - hm, 0u, 0x1010);
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[e][j] = (uint32_t)__viaddmin_s16x2(h[e][j], neg, a.TT);
+            } else {
+#pragma unroll
+                for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
+            }
+        }
+        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, a.G);
+        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, a.G);
+        if (lane_g == 0) up = a.TT;
+        if (lane_g == a.G - 1) dn = a.TT;
+#pragma unroll
+        for (int e = 0; e < 2; ++e) {
+            const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);
+            const uint32_t next7 = prmt(h[e][0], dn, e == 0 ? 0x5432 : 0x7632);
+            uint32_t out[8];
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+                const uint32_t pv = j == 0 ? prev0 : h[e][j - 1];
+                const uint32_t nx = j == 7 ? next7 : h[e][j + 1];
+                out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[e][j]));
+                if (PAD) out[j] &= ~padm[j];
+            }
+            store(kp + e, out);
+        }
+    }
+}
+
+template <typename TD>
+__device__ __forceinline__ void load_d(const TD *p, bool io, uint32_t dv[8])
+{
+    if (io) {
+        DLoad<TD>::load(p, dv);
+    } else {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) dv[j] = 0u;
+    }
+}
+
+constexpr int PAIR_T = 256;  // threads per CTA of k_update_pair
+
+__device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, bool valid)
+{
+    const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(sa), "l"(gsrc), "r"(valid ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// Every global input of a row step is prefetched one step ahead with cp.async into
+// a per-thread staging slot (no registers held, zero-filled where a neighbour does
+// not exist), so the barrier-separated phases never wait on HBM latency:
+//   stage[buf][0..3][tid]   the 4 incoming chunks of the thread's colour-A pixel
+//   stage[buf][4..4+DW)     its D chunk(s);  stage[buf][4+DW..4+2DW)  the colour-B pixel's
+template <typename TD, int MODEA, bool PAD, bool SIGNED>
+__global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD *__restrict__ D, int band)
+{
+    constexpr int DW = sizeof(TD) == 1 ? 1 : 2;  // 16-byte D chunks per lane
+    constexpr int NST = 4 + 2 * DW;
+    extern __shared__ uint4 smem[];
+    // colour-A messages kept UNPACKED (u16x2, two uint4 per lane: no PRMT pack in the
+    // A-phase, no unpack in the B-phase), one buffer per (slot, row) still to be read:
+    // slot 0 of row ya (read by B(ya-1) in the same step), slots 2/3 of rows ya and
+    // ya-1 (B(ya-1), B(ya)), slot 1 of rows ya-2..ya (B(ya-1), B(ya), B(ya+1))
+    constexpr int RB = 2 * PAIR_T;               // uint4 per buffer: [half][PAIR_T]
+    uint4 *ring0 = smem;                         // slot 0
+    uint4 *ring23 = smem + RB;                   // [row & 1][slot 2, 3]
+    uint4 *ring1 = smem + 5 * RB;                // [row % 3]
+    uint4 *stage = smem + 8 * RB;                // [2][NST][PAIR_T]
+    const int NG = PAIR_T >> a.log2G, NI = NG - 2;
+    const int tid = threadIdx.x;
+    const int g = tid >> a.log2G, lane_g = tid & (a.G - 1);
+    const int b = blockIdx.z;
+    const int I0 = blockIdx.x * NI;
+    const int Y0 = blockIdx.y * band, Y1 = min(Y0 + band, a.H);
+    const uint32_t cA = a.colour, cB = a.colour ^ 1u;
+    const bool lio = lane_g < a.nch;
+    const int d0 = lane_g * CH;
+    const uint32_t P = a.plane, Lp = (uint32_t)a.Lp, rowstep = (uint32_t)a.Wc * Lp;
+    const uint8_t *Mr = a.M + (size_t)b * a.pairM;  // colour-B messages of iteration t-1
+    uint8_t *Mw = a.Mw + (size_t)b * a.pairM;       // colour-B messages of iteration t+1
+    const TD *Db = D + (size_t)b * a.pairD;
+
+    uint32_t padm[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        padm[j] = !PAD ? 0u
+                       : (d0 + j >= a.L ? (SIGNED ? 0x00007FFFu : 0x0000FFFFu) : 0u) |
+                             (d0 + j + 8 >= a.L ? (SIGNED ? 0x7FFF0000u : 0xFFFF0000u) : 0u);
+
+    // enqueue the global inputs of step `ya` (A row ya, B row ya-1) into stage[buf]
+    auto issue = [&](int ya, int buf) {
+        uint4 *st = stage + (size_t)buf * NST * PAIR_T + tid;
+        {
+            const bool row = ya >= 0 && ya < a.H;
+            const int i = I0 - 1 + g;
+            const uint32_t o = (cA + (uint32_t)ya) & 1u;
+            const int x = 2 * i + (int)o;
+            const bool io = row && i >= 0 && x < a.W && lio;
+            const bool has[4] = {ya > 0, ya < a.H - 1, x > 0, x < a.W - 1};
+            const uint32_t r = io ? ((uint32_t)ya * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0 : 0u;
+            if (MODEA == 0) {
+                const uint8_t *Mo = Mr + (size_t)(cB * 4u) * P;
+                cp_async16(st + 0 * PAIR_T, Mo + (io && has[0] ? 1u * P + r - rowstep : 0u), io && has[0]);
+                cp_async16(st + 1 * PAIR_T, Mo + (io && has[1] ? r + rowstep : 0u), io && has[1]);
+                cp_async16(st + 2 * PAIR_T, Mo + (io && has[2] ? 3u * P + r + (o - 1u) * Lp : 0u), io && has[2]);
+                cp_async16(st + 3 * PAIR_T, Mo + (io && has[3] ? 2u * P + r + o * Lp : 0u), io && has[3]);
+            } else if (MODEA == 2) {
+                const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
+                const int X = x >> 1, Y = ya >> 1;
+                const int pyu = (ya - 1) >> 1, pyd = (ya + 1) >> 1, pxl = (x - 1) >> 1, pxr = (x + 1) >> 1;
+                const uint32_t Wcp = (uint32_t)a.Wcp;
+#pragma unroll
+                for (int k = 0; k < 4; ++k) {
+                    const int px = k == 2 ? pxl : (k == 3 ? pxr : X);
+                    const int py = k == 0 ? pyu : (k == 1 ? pyd : Y);
+                    const int slot = k ^ 1;
+                    const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
+                    const bool v = io && has[k] && ph;
+                    const uint32_t off = v ? ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
+                                                 ((uint32_t)py * Wcp + (uint32_t)(px >> 1)) * Lp + (uint32_t)d0
+                                           : 0u;
+                    cp_async16(st + k * PAIR_T, Mpb + off, v);
+                }
+            }
+            const uint4 *dp = reinterpret_cast<const uint4 *>(Db + cA * P + r);
+#pragma unroll
+            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + w) * PAIR_T, dp + w, io);
+        }
+        {
+            const int yb = ya - 1;
+            const bool row = yb >= Y0 && yb < Y1;
+            const int i = I0 + g;
+            const uint32_t o = (cB + (uint32_t)yb) & 1u;
+            const int x = 2 * i + (int)o;
+            const bool io = row && g < NI && i < a.Wc && x < a.W && lio;
+            const uint32_t r = io ? ((uint32_t)yb * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0 : 0u;
+            const uint4 *dp = reinterpret_cast<const uint4 *>(Db + cB * P + r);
+#pragma unroll
+            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + DW + w) * PAIR_T, dp + w, io);
+        }
+        cp_async_commit();
+    };
+
+    issue(Y0 - 1, 0);
+    int s = 0;
+#pragma unroll 1
+    for (int ya = Y0 - 1; ya <= Y1; ++ya, ++s) {
+        cp_async_wait_all();  // this step's inputs (this thread's own copies)
+        if (ya + 1 <= Y1) issue(ya + 1, (s + 1) & 1);
+        const uint4 *st = stage + (size_t)(s & 1) * NST * PAIR_T + tid;
+        // ---- A-phase: colour-A pixel index I0-1+g of row ya (incl. the halo pixels)
+        if (ya >= 0 && ya < a.H) {
+            const int i = I0 - 1 + g;
+            const uint32_t o = (cA + (uint32_t)ya) & 1u;
+            const int x = 2 * i + (int)o;
+            const bool io = i >= 0 && x < a.W && lio;
+            uint32_t dv[8], in[4][8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) unpack_u8(MODEA == 1 ? make_uint4(0u, 0u, 0u, 0u) : st[k * PAIR_T], in[k]);
+            if (sizeof(TD) == 1) {
+                unpack_u8(st[4 * PAIR_T], dv);
+            } else {
+                const uint4 lo = st[4 * PAIR_T], hi = st[5 * PAIR_T];
+                dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
+                dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
+            }
+            (void)io;  // staged chunks of pixels outside the image are zero
+            uint4 *const dst[4] = {ring0 + tid, ring1 + (size_t)((ya + 3) % 3) * RB + tid,
+                                   ring23 + (size_t)((ya & 1) * 2 + 0) * RB + tid,
+                                   ring23 + (size_t)((ya & 1) * 2 + 1) * RB + tid};
+            outgoing<PAD, SIGNED>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
+                dst[k][0] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+                dst[k][PAIR_T] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+            });
+        }
+        __syncthreads();
+        // ---- B-phase: colour-B pixel index I0+g of row yb = ya-1, from the ring
+        const int yb = ya - 1;
+        if (yb >= Y0 && yb < Y1) {  // block-uniform: every lane takes part in the group shuffles
+            const int i = I0 + g;
+            const uint32_t o = (cB + (uint32_t)yb) & 1u;
+            const int x = 2 * i + (int)o;
+            const bool io = g < NI && i < a.Wc && x < a.W && lio;
+            const bool has[4] = {yb > 0, yb < a.H - 1, x > 0, x < a.W - 1};
+            const uint32_t r = ((uint32_t)yb * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0;
+            // A(i, yb-1) sends down (slot 1), A(i, yb+1) up (slot 0), A(i-1+o, yb) right
+            // (slot 3), A(i+o, yb) left (slot 2); the group of A index j is j - (I0 - 1)
+            const uint4 *src[4] = {ring1 + (size_t)((yb + 2) % 3) * RB + (g + 1) * a.G + lane_g,
+                                   ring0 + (g + 1) * a.G + lane_g,
+                                   ring23 + (size_t)((yb & 1) * 2 + 1) * RB + (g + (int)o) * a.G + lane_g,
+                                   ring23 + (size_t)((yb & 1) * 2 + 0) * RB + (g + 1 + (int)o) * a.G + lane_g};
+            uint32_t dv[8], in[4][8];
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                const bool v = io && has[k];
+                const uint4 lo = v ? src[k][0] : make_uint4(0u, 0u, 0u, 0u);
+                const uint4 hi = v ? src[k][PAIR_T] : make_uint4(0u, 0u, 0u, 0u);
+                in[k][0] = lo.x, in[k][1] = lo.y, in[k][2] = lo.z, in[k][3] = lo.w;
+                in[k][4] = hi.x, in[k][5] = hi.y, in[k][6] = hi.z, in[k][7] = hi.w;
+            }
+            if (sizeof(TD) == 1) {
+                unpack_u8(st[(4 + DW) * PAIR_T], dv);
+            } else {
+                const uint4 lo = st[(4 + DW) * PAIR_T], hi = st[(5 + DW) * PAIR_T];
+                dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
+                dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
+            }
+            uint8_t *Mo = Mw + (size_t)(cB * 4u) * P + r;
+            outgoing<PAD, SIGNED>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
+                if (io) *reinterpret_cast<uint4 *>(Mo + (size_t)k * P) = pack_u8(o8);
+            });
+        }
+        __syncthreads();
+    }
+}
+
+size_t pair_smem_bytes(int dbytes)
+{
+    const int DW = dbytes == 1 ? 1 : 2;
+    return (size_t)(8 * 2 + 2 * (4 + 2 * DW)) * PAIR_T * sizeof(uint4);
+}
+
+cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,
+                               cudaStream_t st)
+{
+    const int NI = (PAIR_T >> a.log2G) - 2;
+    dim3 grid((unsigned)((a.Wc + NI - 1) / NI), (unsigned)((a.H + band - 1) / band), (unsigned)B);
+    const size_t smem = pair_smem_bytes(dbytes);
+    const bool pad = (a.L % CH) != 0 || a.G != a.nch;
+#define VSBP_K(TD_, MODE_, PAD_, SG_)                                                                           \
+    do {                                                                                                        \
+        auto kf = k_update_pair<TD_, MODE_, PAD_, SG_>;                                                         \
+        static cudaError_t attr = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (attr != cudaSuccess) return attr;                                                                   \
+        kf<<<grid, PAIR_T, smem, st>>>(a, (const TD_ *)D, band);                                                \
+    } while (0)
+#define VSBP_S(TD_, MODE_, PAD_) \
+    if (sgn) VSBP_K(TD_, MODE_, PAD_, true); else VSBP_K(TD_, MODE_, PAD_, false);
+#define VSBP_P(TD_, MODE_) \
+    if (pad) { VSBP_S(TD_, MODE_, true) } else { VSBP_S(TD_, MODE_, false) }
+#define VSBP_M(TD_)              \
+    switch (mode) {              \
+    case 0: VSBP_P(TD_, 0) break; \
+    case 1: VSBP_P(TD_, 1) break; \
+    default: VSBP_P(TD_, 2) break; \
+    }
+    if (dbytes == 1) {
+        VSBP_M(uint8_t)
+    } else {
+        VSBP_M(uint16_t)
+    }
+#undef VSBP_M
+#undef VSBP_P
+#undef VSBP_S
+#undef VSBP_K
+    note_launch();
+    return cudaGetLastError();
+}
+
 cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
                                cudaStream_t st)
 {

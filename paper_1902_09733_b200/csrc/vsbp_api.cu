@@ -22,10 +22,13 @@ struct vsbp_bp {
     int dimg;  // level-0 data term computed from the images inside the update (no D_0 traffic)
     int final_fuse;  // VSBP_OPT_FINAL: last level-0 iteration fused with the WTA (messages not stored)
     int final_ran;   // the last call fused it: level-0 messages of the last colour are stale
+    int pair_fuse;   // VSBP_OPT_PAIR: two checkerboard iterations per launch (k_update_pair)
+    int pair_band;   // rows per CTA band of k_update_pair
+    int mcur[16];    // which of the level's two message arrays holds its current messages
     int Wl[16], Hl[16], Wcl[16];
     int dbytes[16];
     // workspace plan (bytes) for ws_batch pairs
-    size_t d_off[16], m_off[16], total;
+    size_t d_off[16], m_off[16], m2_off[16], total;  // m2_off: the second message array (0: none)
     void *ws;
     size_t ws_bytes;
     int ws_batch;
@@ -72,6 +75,8 @@ int bytes_for_max(long long vmax)
 
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
+bool use_pair(const vsbp_bp *c, int l);
+
 void plan(vsbp_bp *c, int batch)
 {
     size_t off = 0;
@@ -83,7 +88,20 @@ void plan(vsbp_bp *c, int batch)
         c->m_off[l] = off;
         off = align256(off + (size_t)batch * 8 * c->Hl[l] * c->Wcl[l] * c->Lp * c->msg_bytes);
     }
+    for (int l = 0; l < c->levels; ++l) {
+        c->m2_off[l] = 0;
+        if (use_pair(c, l)) {
+            c->m2_off[l] = off;
+            off = align256(off + (size_t)batch * 8 * c->Hl[l] * c->Wcl[l] * c->Lp * c->msg_bytes);
+        }
+    }
     c->total = off;
+}
+
+// the level's current message array (k_update_pair ping-pongs between two)
+inline char *msg_base(const vsbp_bp *c, char *ws, int l)
+{
+    return ws + (c->mcur[l] ? c->m2_off[l] : c->m_off[l]);
 }
 
 vsbp::Geom geom(const vsbp_bp *c, int B, int l)
@@ -128,6 +146,20 @@ bool use_final(const vsbp_bp *c)
     return c->final_fuse && use_fast(c, 0) && !use_dimg(c) && c->dbytes[0] == 1 && c->iters >= 2 && c->W >= 2;
 }
 
+// two iterations per launch (k_update_pair): the packed kernel with D from memory,
+// at least three iterations (the last one of every level stays a single launch: its
+// messages must all be stored -- the WTA, the up-copy and the exports read both
+// colours), and one Lp chunk per lane group that fits the CTA
+bool use_pair(const vsbp_bp *c, int l)
+{
+    if (!c->pair_fuse || !use_fast(c, l) || c->iters < 3 || c->G > 32) return false;
+    if (l == 0 && use_dimg(c)) return false;
+    // 1 (default): levels of >= 100K pixels only -- a CTA walks its band row by row,
+    // so small levels have too few CTAs to fill the GPU (levels 2-4 of C2 measured
+    // 1.8-2.3x slower fused); 2: every level (tests)
+    return c->pair_fuse == 2 || (long long)c->Wl[l] * c->Hl[l] >= 100000;
+}
+
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
 bool fast_signed(const vsbp_bp *c, int l)
 {
@@ -139,8 +171,9 @@ vsbp::FastArgs fast_args(const vsbp_bp *c, int l, char *ws, int32_t *disp)
 {
     vsbp::FastArgs a;
     const int lp = l + 1 < c->levels ? l + 1 : l;
-    a.M = (uint8_t *)(ws + c->m_off[l]);
-    a.Mp = (const uint8_t *)(ws + c->m_off[lp]);
+    a.M = (uint8_t *)msg_base(c, ws, l);
+    a.Mw = c->m2_off[l] ? (uint8_t *)(ws + (c->mcur[l] ? c->m_off[l] : c->m2_off[l])) : nullptr;
+    a.Mp = (const uint8_t *)msg_base(c, ws, lp);
     a.disp = disp;
     a.W = c->Wl[l];
     a.H = c->Hl[l];
@@ -266,6 +299,12 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
     c->msg_bytes = bytes_for_max(c->tau_q);
     c->dimg = 0;  // measured slower (ALU-bound): DESIGN.md §12
     c->final_fuse = 0;  // measured slower (4x the unpack/sum work per colour-A pixel): DESIGN.md §12
+    c->pair_fuse = 1;
+    c->pair_band = 64;
+    for (int l = 0; l < 16; ++l) {
+        c->mcur[l] = 0;
+        c->m2_off[l] = 0;
+    }
     c->final_ran = 0;
     *out = c;
     return VSBP_OK;
@@ -297,6 +336,18 @@ int bp_set_option(vsbp_bp *c, int option, int value)
     if (option == VSBP_OPT_FINAL) {
         if (value < 0 || value > 2) return VSBP_EINVAL;
         c->final_fuse = value;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_PAIR) {
+        if (value < 0 || value > 2) return VSBP_EINVAL;
+        c->pair_fuse = value;
+        c->ws = nullptr;  // plan changes (second message arrays): workspace must be re-bound
+        c->ws_batch = 0;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_PAIR_BAND) {
+        if (value < 1 || value > 4096) return VSBP_EINVAL;
+        c->pair_band = value;
         return VSBP_OK;
     }
     return VSBP_EINVAL;
@@ -402,8 +453,9 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
     for (int l = top; l >= 0; --l) {
         vsbp::Geom g = geom(c, B, l);
         void *D = ws + c->d_off[l];
-        void *M = ws + c->m_off[l];
-        const void *Mp = (l < top) ? (const void *)(ws + c->m_off[l + 1]) : nullptr;
+        c->mcur[l] = 0;
+        void *M = msg_base(c, ws, l);
+        const void *Mp = (l < top) ? (const void *)msg_base(c, ws, l + 1) : nullptr;
         if (c->iters == 1) {
             // colour 1 is never updated on this level: materialise its initial
             // messages (0 at the top, the parent's otherwise), R-12
@@ -418,9 +470,36 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         const int slot = c->timing ? (c->ev_head + c->n_pending++) % EV_RING : -1;
         if (slot >= 0) CK(cudaEventRecord(c->ev[slot][0], st));
         double bytes = 0.0;
+        int launches = 0;
         const bool fast = use_fast(c, l);
         for (int t = 0; t < c->iters; ++t) {
             const int mode = (t > 0) ? 0 : (l == top ? 1 : 2);
+            if (fast && use_pair(c, l) && t + 1 < c->iters - 1) {
+                // iterations t and t+1 in one launch; the level's messages move to its
+                // other array (colour t&1's are consumed on chip and never stored)
+                vsbp::FastArgs fa = fast_args(c, l, ws, disp);
+                fa.colour = (uint32_t)(t & 1);
+                CK(vsbp::launch_update_pair(D, c->dbytes[l], fa, B, mode, fast_signed(c, l), c->pair_band, st));
+                c->mcur[l] ^= 1;
+                long long nA = 0, nB = 0;
+                for (int y = 0; y < g.H; ++y) {
+                    nA += (g.W + (((t + y) & 1) ? 0 : 1)) / 2;
+                    nB += (g.W + (((t + 1 + y) & 1) ? 0 : 1)) / 2;
+                }
+                // D of both colours + colour B's 4 messages out (+ its 4 in for MODE 0;
+                // the parent's planes once for MODE 2)
+                double by = (double)(nA + nB) * c->L * c->dbytes[l] + (double)nB * 4.0 * c->L * c->msg_bytes;
+                if (mode == 0) by += (double)nB * 4.0 * c->L * c->msg_bytes;
+                if (mode == 2) {
+                    const vsbp::Geom gp = geom(c, B, l + 1);
+                    by += (double)gp.W * gp.H * 4.0 * c->L * c->msg_bytes;
+                }
+                bytes += (double)B * by;
+                ++launches;
+                ++t;  // the pair covered t+1 too
+                continue;
+            }
+            ++launches;
             if (fast) {
                 vsbp::FastArgs fa = fast_args(c, l, ws, disp);
                 fa.colour = (uint32_t)(t & 1);
@@ -469,7 +548,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         if (slot >= 0) {
             CK(cudaEventRecord(c->ev[slot][1], st));
             c->ev_level[slot] = l;
-            c->ev_launches[slot] = c->iters;
+            c->ev_launches[slot] = launches;
             c->ev_bytes[slot] = bytes;
         }
     }
@@ -489,7 +568,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
             CK(vsbp::launch_update_fast(ws + c->d_off[0], db, fa, B, 3, true, false, st));
         } else {
             vsbp::Geom g = geom(c, B, 0);
-            CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], ws + c->m_off[0], c->msg_bytes, g, disp, -1, st));
+            CK(vsbp::launch_wta(ws + c->d_off[0], c->dbytes[0], msg_base(c, ws, 0), c->msg_bytes, g, disp, -1, st));
         }
     }
     c->last_B = B;
@@ -510,7 +589,7 @@ int bp_get_messages(vsbp_bp *c, int pair, int level, int32_t *out, void *stream)
     if (!c->ws || pair >= c->ws_batch) return VSBP_EDIM;
     plan(c, c->ws_batch);
     vsbp::Geom g = geom(c, c->ws_batch, level);
-    CK(vsbp::launch_export_msgs(wsp(c) + c->m_off[level], c->msg_bytes, g, pair, out, (cudaStream_t)stream));
+    CK(vsbp::launch_export_msgs(msg_base(c, wsp(c), level), c->msg_bytes, g, pair, out, (cudaStream_t)stream));
     return VSBP_OK;
 }
 

@@ -38,6 +38,7 @@ cudaError_t launch_wta(const void *D, int dbytes, const void *M, int mbytes, con
 // arguments of the packed update kernel (bp_fast.cu); offsets are per pair, in elements
 struct FastArgs {
     uint8_t *M;        // this level's messages
+    uint8_t *Mw;       // k_update_pair: the level's other message array (colour-B output)
     const uint8_t *Mp; // parent level's messages (MODE 2)
     int32_t *disp;     // WTA output (fused WTA / MODE 3)
     uint32_t npix;     // H * Wc (pixels of one colour)
@@ -56,6 +57,12 @@ struct FastArgs {
 // dbytes 1 / 2: D is u8 / u16; dbytes 0: level 0 computed from a.gl / a.gr (ImgD)
 cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool wta, bool sgn,
                                cudaStream_t st);
+// two checkerboard iterations (a.colour, then its complement) in one launch, reading
+// a.M (or the parent, mode 2; nothing, mode 1) and writing the second colour's
+// messages to a.Mw; rows per CTA band
+cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,
+                               cudaStream_t st);
+size_t pair_smem_bytes(int dbytes);
 // fused last level-0 iteration + WTA of both colours (a.colour = the colour updated last)
 cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);
 cudaError_t launch_final_tile(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);

@@ -78,15 +78,19 @@ def test_level_dims_and_workspace():
         assert L.bp_level_dims(h, l, C.byref(w), C.byref(hh)) == 0
         dims.append((w.value, hh.value))
     assert dims == oracle.level_dims(676, 380, 5)
+    n1p = L.bp_workspace_bytes(h, 1)  # default: two iterations per launch -> a second u8 message array per level
+    assert L.bp_set_option(h, P.VSBP_OPT_PAIR, 0) == 0
     n1 = L.bp_workspace_bytes(h, 1)
     n4 = L.bp_workspace_bytes(h, 4)
     assert n1 > 0 and n4 >= 4 * n1 - 4096 * 10
+    msgs = sum(8 * h_ * ((w_ + 1) // 2) * 64 for w_, h_ in dims if w_ * h_ >= 100000)  # one u8 array per large level
+    assert msgs - 256 * 5 <= n1p - n1 <= msgs + 256 * 5
     # message option: narrower than lossless is refused, wider accepted
     assert L.bp_set_option(h, P.VSBP_OPT_MSG_BYTES, 2) == 0
     assert L.bp_workspace_bytes(h, 1) > n1
     assert L.bp_set_option(h, P.VSBP_OPT_MSG_BYTES, 3) == -1
     # 0/1 switches; anything else (or an unknown option) is refused
-    for opt, top in ((P.VSBP_OPT_KERNEL, 1), (P.VSBP_OPT_DIMG, 1), (P.VSBP_OPT_FINAL, 2)):
+    for opt, top in ((P.VSBP_OPT_KERNEL, 1), (P.VSBP_OPT_DIMG, 1), (P.VSBP_OPT_FINAL, 2), (P.VSBP_OPT_PAIR, 2)):
         assert all(L.bp_set_option(h, opt, v) == 0 for v in range(top + 1))
         assert L.bp_set_option(h, opt, top + 1) == -1 and L.bp_set_option(h, opt, -1) == -1
     assert L.bp_set_option(h, 99, 0) == -1

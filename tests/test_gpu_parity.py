@@ -22,14 +22,17 @@ def to_dev(a):
     return torch.from_numpy(np.ascontiguousarray(a)).to(dev())
 
 
-def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, batch=None, final=0):
+def run_gpu_bp(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_bytes=0, batch=None, final=0,
+               pair=2):
+    """pair=2: two iterations per launch on EVERY eligible level (the default, 1,
+    fuses only levels of >= 100K pixels, which small test images never reach)."""
     left = np.asarray(left)
     right = np.asarray(right)
     if left.ndim == 2:
         left, right = left[None], right[None]
     B, H, W = left.shape
     bp = P.StereoBP(W, H, L, levels, iters, lam, dt, st, batch=batch or B, msg_bytes=msg_bytes, device=dev(),
-                    final=final)
+                    final=final, pair=pair)
     disp = bp.disparity(to_dev(left), to_dev(right))
     torch.cuda.synchronize()
     return bp, disp.cpu().numpy()
@@ -40,6 +43,8 @@ def check_bp_case(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_
     default stored-message path, whose messages are compared on every level."""
     bp, disp = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes)
     d_o, msgs_o = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
+    _, disp_1 = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, pair=0)
+    assert np.array_equal(disp_1[0], d_o), "disparity differs (one iteration per launch)"
     for variant in (1, 2):
         _, disp_f = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, final=variant)
         assert np.array_equal(disp_f[0], d_o), f"disparity differs (fused final iteration, variant {variant})"
