@@ -3,21 +3,21 @@
 #   tools/final_round.sh TAG
 # 1) all GPU tests, 2) smoke(), 3) the default bench line (N=1, cpu_baseline, e2e),
 # 4) the reference (oracle) arm, 5) f-row timings, 6) the ncu launch list of the
-# bench command and one --set full capture each of the level-0 update, JBU and
-# cost-volume kernels.  Every step runs without ncu first.  Outputs in gpurun_out/.
+# bench command and one --set full capture each of the two-iteration and single
+# level-0 updates, the JBU and the compaction write.  Every step runs without ncu
+# first.  Outputs in gpurun_out/.
 TAG=${1:-final}
 mkdir -p gpurun_out
 python -c "from paper_1902_09733_b200 import build as B; B.build()" || exit 1
-timeout 900 python -m pytest tests -m gpu -q > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$TAG.log
+timeout 1200 python -m pytest tests -m gpu -q > gpurun_out/pytest_$TAG.log 2>&1; echo "pytest rc=$?"; tail -1 gpurun_out/pytest_$TAG.log
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke_$TAG.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke_$TAG.log
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
-timeout 900 python tools/bench_rows.py --out gpurun_out/rows_$TAG.json > /dev/null 2> gpurun_out/rows_$TAG.err; echo "rows rc=$?"
-timeout 300 python tools/time_icp.py > gpurun_out/icp_$TAG.json 2>&1; echo "icp rc=$?"
-ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pool 1"
+[ -n "$SKIP_ROWS" ] || { timeout 900 python tools/bench_rows.py --out gpurun_out/rows_$TAG.json > /dev/null 2> gpurun_out/rows_$TAG.err; echo "rows rc=$?"; }
+ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 256"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
-for cap in k_update_fast:21 k_jbu_vec:1 k_costpyr_fast:1; do
+for cap in ${CAPS:-k_update_pair:3 k_update_fast:8 k_jbu_vec:1 k_compact_write:1}; do
     K=${cap%%:*}; S=${cap##*:}
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
         -o gpurun_out/prof_${TAG}_$K python bench.py $ARGS > gpurun_out/ncu_full_${TAG}_$K.log 2>&1
