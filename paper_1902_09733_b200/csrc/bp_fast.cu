@@ -661,10 +661,11 @@ cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn,
 // arithmetic per pixel is k_update_fast's, so the messages are bit-identical.
 // The colour-A halo (2 pixels per 64-pixel tile row, 2 rows per band) is computed
 // twice.  Requires TD = u8 / u16 D, u8 messages (the fast-kernel domain).
-template <bool PAD, bool SIGNED, typename Store>
+template <bool PAD, bool SIGNED, int GT, typename Store>
 __device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8], const uint32_t (&in)[4][8],
                                          const uint32_t padm[8], int lane_g, Store store)
 {
+    const int G = GT ? GT : a.G;  // lanes per pixel (compile-time for the common L)
 #pragma unroll
     for (int kp = 0; kp < 4; kp += 2) {
         uint32_t h[2][8];
@@ -679,7 +680,8 @@ __device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8]
             }
         }
         uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
-        for (int s = a.G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, a.G));
+#pragma unroll
+        for (int s = G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, G));
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
@@ -692,10 +694,10 @@ __device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8]
                 for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
             }
         }
-        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, a.G);
-        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, a.G);
+        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, G);
+        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, G);
         if (lane_g == 0) up = a.TT;
-        if (lane_g == a.G - 1) dn = a.TT;
+        if (lane_g == G - 1) dn = a.TT;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);
@@ -739,9 +741,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // not exist), so the barrier-separated phases never wait on HBM latency:
 //   stage[buf][0..3][tid]   the 4 incoming chunks of the thread's colour-A pixel
 //   stage[buf][4..4+DW)     its D chunk(s);  stage[buf][4+DW..4+2DW)  the colour-B pixel's
-template <typename TD, int MODEA, bool PAD, bool SIGNED>
+template <typename TD, int MODEA, bool PAD, bool SIGNED, int GT>
 __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD *__restrict__ D, int band)
 {
+    const int G = GT ? GT : a.G, LOG2G = GT == 1 ? 0 : GT == 2 ? 1 : GT == 4 ? 2 : GT == 8 ? 3 : a.log2G;
     constexpr int DW = sizeof(TD) == 1 ? 1 : 2;  // 16-byte D chunks per lane
     constexpr int NST = 4 + 2 * DW;
     extern __shared__ uint4 smem[];
@@ -754,9 +757,9 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
     uint4 *ring23 = smem + RB;                   // [row & 1][slot 2, 3]
     uint4 *ring1 = smem + 5 * RB;                // [row % 3]
     uint4 *stage = smem + 8 * RB;                // [2][NST][PAIR_T]
-    const int NG = PAIR_T >> a.log2G, NI = NG - 2;
+    const int NG = PAIR_T >> LOG2G, NI = NG - 2;
     const int tid = threadIdx.x;
-    const int g = tid >> a.log2G, lane_g = tid & (a.G - 1);
+    const int g = tid >> LOG2G, lane_g = tid & (G - 1);
     const int b = blockIdx.z;
     const int I0 = blockIdx.x * NI;
     const int Y0 = blockIdx.y * band, Y1 = min(Y0 + band, a.H);
@@ -856,7 +859,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
             uint4 *const dst[4] = {ring0 + tid, ring1 + (size_t)((ya + 3) % 3) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 0) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 1) * RB + tid};
-            outgoing<PAD, SIGNED>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
+            outgoing<PAD, SIGNED, GT>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
                 dst[k][0] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
                 dst[k][PAIR_T] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
             });
@@ -873,10 +876,10 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
             const uint32_t r = ((uint32_t)yb * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0;
             // A(i, yb-1) sends down (slot 1), A(i, yb+1) up (slot 0), A(i-1+o, yb) right
             // (slot 3), A(i+o, yb) left (slot 2); the group of A index j is j - (I0 - 1)
-            const uint4 *src[4] = {ring1 + (size_t)((yb + 2) % 3) * RB + (g + 1) * a.G + lane_g,
-                                   ring0 + (g + 1) * a.G + lane_g,
-                                   ring23 + (size_t)((yb & 1) * 2 + 1) * RB + (g + (int)o) * a.G + lane_g,
-                                   ring23 + (size_t)((yb & 1) * 2 + 0) * RB + (g + 1 + (int)o) * a.G + lane_g};
+            const uint4 *src[4] = {ring1 + (size_t)((yb + 2) % 3) * RB + (g + 1) * G + lane_g,
+                                   ring0 + (g + 1) * G + lane_g,
+                                   ring23 + (size_t)((yb & 1) * 2 + 1) * RB + (g + (int)o) * G + lane_g,
+                                   ring23 + (size_t)((yb & 1) * 2 + 0) * RB + (g + 1 + (int)o) * G + lane_g};
             uint32_t dv[8], in[4][8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
@@ -894,7 +897,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
             uint8_t *Mo = Mw + (size_t)(cB * 4u) * P + r;
-            outgoing<PAD, SIGNED>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
+            outgoing<PAD, SIGNED, GT>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
                 if (io) *reinterpret_cast<uint4 *>(Mo + (size_t)k * P) = pack_u8(o8);
             });
         }
@@ -915,12 +918,19 @@ cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int
     dim3 grid((unsigned)((a.Wc + NI - 1) / NI), (unsigned)((a.H + band - 1) / band), (unsigned)B);
     const size_t smem = pair_smem_bytes(dbytes);
     const bool pad = (a.L % CH) != 0 || a.G != a.nch;
-#define VSBP_K(TD_, MODE_, PAD_, SG_)                                                                           \
+#define VSBP_KG(TD_, MODE_, PAD_, SG_, GT_)                                                                     \
     do {                                                                                                        \
-        auto kf = k_update_pair<TD_, MODE_, PAD_, SG_>;                                                         \
+        auto kf = k_update_pair<TD_, MODE_, PAD_, SG_, GT_>;                                                    \
         static cudaError_t attr = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (attr != cudaSuccess) return attr;                                                                   \
         kf<<<grid, PAIR_T, smem, st>>>(a, (const TD_ *)D, band);                                                \
+    } while (0)
+    // the lane-group size is a compile-time constant for L = 64 (G = 4) and L = 128 (G = 8)
+#define VSBP_K(TD_, MODE_, PAD_, SG_)                                   \
+    do {                                                                \
+        if (!PAD_ && a.G == 4) VSBP_KG(TD_, MODE_, PAD_, SG_, 4);       \
+        else if (!PAD_ && a.G == 8) VSBP_KG(TD_, MODE_, PAD_, SG_, 8);  \
+        else VSBP_KG(TD_, MODE_, PAD_, SG_, 0);                         \
     } while (0)
 #define VSBP_S(TD_, MODE_, PAD_) \
     if (sgn) VSBP_K(TD_, MODE_, PAD_, true); else VSBP_K(TD_, MODE_, PAD_, false);
