@@ -95,18 +95,21 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        u8 level-0 costs, iters >= 2 and W >= 2. */
 #define VSBP_OPT_FINAL 4
 /*   VSBP_OPT_PAIR      : 1 (default) = two checkerboard iterations per launch on
- *                        levels of >= 100K pixels where the packed kernel runs with
+ *                        large levels where the packed kernel runs with
  *                        D from memory and the level has >= 3 iterations (all but
  *                        its last iteration go in pairs): the first colour's
  *                        messages stay on chip, so a pair moves 10L instead of 18L
- *                        bytes per pixel pair at u8.  The level's messages then
+ *                        bytes per pixel pair at u8 (levels >= VSBP_OPT_PAIR_MINPX).  The level's messages then
  *                        alternate between two arrays (bp_workspace_bytes grows by
  *                        one message array per such level).  2 = on every eligible
  *                        level (tests); 0 = one iteration per launch.  Results are
  *                        identical.
- *   VSBP_OPT_PAIR_BAND : rows per CTA of the two-iteration kernel (default 64). */
+ *   VSBP_OPT_PAIR_BAND : rows per CTA of the two-iteration kernel (default 64).
+ *   VSBP_OPT_PAIR_MINPX: smallest level (W_l * H_l pixels) fused under
+ *                        VSBP_OPT_PAIR = 1 (default 100000). */
 #define VSBP_OPT_PAIR 5
 #define VSBP_OPT_PAIR_BAND 6
+#define VSBP_OPT_PAIR_MINPX 7
 int bp_set_option(vsbp_bp *ctx, int option, int value);
 
 /* Quantised parameters: out[0..7] = {lambda_q, tau_d, tau_q, S, msg_bytes,

@@ -34,6 +34,7 @@ VSBP_OPT_DIMG = 3
 VSBP_OPT_FINAL = 4
 VSBP_OPT_PAIR = 5
 VSBP_OPT_PAIR_BAND = 6
+VSBP_OPT_PAIR_MINPX = 7
 _ERRNAMES = {-1: "VSBP_EINVAL", -2: "VSBP_EDIM", -3: "VSBP_EOVERFLOW", -4: "VSBP_ECUDA"}
 
 
@@ -171,6 +172,9 @@ class StereoBP:
             pair_band = int(os.environ["VSBP_PAIR_BAND"])
         if pair_band:
             _check(lib().bp_set_option(self._h, VSBP_OPT_PAIR_BAND, int(pair_band)), "bp_set_option")
+        if os.environ.get("VSBP_PAIR_MINPX"):  # experiment knob
+            _check(lib().bp_set_option(self._h, VSBP_OPT_PAIR_MINPX, int(os.environ["VSBP_PAIR_MINPX"])),
+                   "bp_set_option")
         self.W, self.H, self.L, self.levels, self.iters, self.batch = W, H, ndisp, levels, iters, batch
         nbytes = int(lib().bp_workspace_bytes(self._h, batch))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=device)

@@ -752,7 +752,9 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
     // A-phase, no unpack in the B-phase), one buffer per (slot, row) still to be read:
     // slot 0 of row ya (read by B(ya-1) in the same step), slots 2/3 of rows ya and
     // ya-1 (B(ya-1), B(ya)), slot 1 of rows ya-2..ya (B(ya-1), B(ya), B(ya+1))
-    constexpr int RB = 2 * PAIR_T;               // uint4 per buffer: [half][PAIR_T]
+    // (u16 costs need 2x the staging, so their ring stays packed u8: 2 CTAs per SM either way)
+    constexpr bool UNPK = sizeof(TD) == 1;
+    constexpr int RB = (UNPK ? 2 : 1) * PAIR_T;  // uint4 per buffer: [half][PAIR_T]
     uint4 *ring0 = smem;                         // slot 0
     uint4 *ring23 = smem + RB;                   // [row & 1][slot 2, 3]
     uint4 *ring1 = smem + 5 * RB;                // [row % 3]
@@ -860,8 +862,12 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                                    ring23 + (size_t)((ya & 1) * 2 + 0) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 1) * RB + tid};
             outgoing<PAD, SIGNED, GT>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
-                dst[k][0] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
-                dst[k][PAIR_T] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+                if (UNPK) {
+                    dst[k][0] = make_uint4(o8[0], o8[1], o8[2], o8[3]);
+                    dst[k][PAIR_T] = make_uint4(o8[4], o8[5], o8[6], o8[7]);
+                } else {
+                    dst[k][0] = pack_u8(o8);
+                }
             });
         }
         __syncthreads();
@@ -884,10 +890,14 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
 #pragma unroll
             for (int k = 0; k < 4; ++k) {
                 const bool v = io && has[k];
-                const uint4 lo = v ? src[k][0] : make_uint4(0u, 0u, 0u, 0u);
-                const uint4 hi = v ? src[k][PAIR_T] : make_uint4(0u, 0u, 0u, 0u);
-                in[k][0] = lo.x, in[k][1] = lo.y, in[k][2] = lo.z, in[k][3] = lo.w;
-                in[k][4] = hi.x, in[k][5] = hi.y, in[k][6] = hi.z, in[k][7] = hi.w;
+                if (UNPK) {
+                    const uint4 lo = v ? src[k][0] : make_uint4(0u, 0u, 0u, 0u);
+                    const uint4 hi = v ? src[k][PAIR_T] : make_uint4(0u, 0u, 0u, 0u);
+                    in[k][0] = lo.x, in[k][1] = lo.y, in[k][2] = lo.z, in[k][3] = lo.w;
+                    in[k][4] = hi.x, in[k][5] = hi.y, in[k][6] = hi.z, in[k][7] = hi.w;
+                } else {
+                    unpack_u8(v ? src[k][0] : make_uint4(0u, 0u, 0u, 0u), in[k]);
+                }
             }
             if (sizeof(TD) == 1) {
                 unpack_u8(st[(4 + DW) * PAIR_T], dv);
@@ -908,7 +918,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
 size_t pair_smem_bytes(int dbytes)
 {
     const int DW = dbytes == 1 ? 1 : 2;
-    return (size_t)(8 * 2 + 2 * (4 + 2 * DW)) * PAIR_T * sizeof(uint4);
+    return (size_t)(8 * (dbytes == 1 ? 2 : 1) + 2 * (4 + 2 * DW)) * PAIR_T * sizeof(uint4);
 }
 
 cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,

@@ -24,6 +24,7 @@ struct vsbp_bp {
     int final_ran;   // the last call fused it: level-0 messages of the last colour are stale
     int pair_fuse;   // VSBP_OPT_PAIR: two checkerboard iterations per launch (k_update_pair)
     int pair_band;   // rows per CTA band of k_update_pair
+    long long pair_min_px;  // VSBP_OPT_PAIR = 1: fuse levels of at least this many pixels
     int mcur[16];    // which of the level's two message arrays holds its current messages
     int Wl[16], Hl[16], Wcl[16];
     int dbytes[16];
@@ -154,10 +155,10 @@ bool use_pair(const vsbp_bp *c, int l)
 {
     if (!c->pair_fuse || !use_fast(c, l) || c->iters < 3 || c->G > 32) return false;
     if (l == 0 && use_dimg(c)) return false;
-    // 1 (default): levels of >= 100K pixels only -- a CTA walks its band row by row,
+    // 1 (default): levels of >= pair_min_px pixels only -- a CTA walks its band row by row,
     // so small levels have too few CTAs to fill the GPU (levels 2-4 of C2 measured
     // 1.8-2.3x slower fused); 2: every level (tests)
-    return c->pair_fuse == 2 || (long long)c->Wl[l] * c->Hl[l] >= 100000;
+    return c->pair_fuse == 2 || (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px;
 }
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
@@ -301,6 +302,7 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
     c->final_fuse = 0;  // measured slower (4x the unpack/sum work per colour-A pixel): DESIGN.md §12
     c->pair_fuse = 1;
     c->pair_band = 64;
+    c->pair_min_px = 100000;
     for (int l = 0; l < 16; ++l) {
         c->mcur[l] = 0;
         c->m2_off[l] = 0;
@@ -348,6 +350,13 @@ int bp_set_option(vsbp_bp *c, int option, int value)
     if (option == VSBP_OPT_PAIR_BAND) {
         if (value < 1 || value > 4096) return VSBP_EINVAL;
         c->pair_band = value;
+        return VSBP_OK;
+    }
+    if (option == VSBP_OPT_PAIR_MINPX) {
+        if (value < 0) return VSBP_EINVAL;
+        c->pair_min_px = value;
+        c->ws = nullptr;  // plan changes: workspace must be re-bound
+        c->ws_batch = 0;
         return VSBP_OK;
     }
     return VSBP_EINVAL;
