@@ -99,7 +99,8 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        D from memory and the level has >= 3 iterations (all but
  *                        its last iteration go in pairs): the first colour's
  *                        messages stay on chip, so a pair moves 10L instead of 18L
- *                        bytes per pixel pair at u8 (levels >= VSBP_OPT_PAIR_MINPX).  The level's messages then
+ *                        bytes per pixel pair at u8 (levels with u8 costs and >=
+ *                        VSBP_OPT_PAIR_MINPX pixels).  The level's messages then
  *                        alternate between two arrays (bp_workspace_bytes grows by
  *                        one message array per such level).  2 = on every eligible
  *                        level (tests); 0 = one iteration per launch.  Results are

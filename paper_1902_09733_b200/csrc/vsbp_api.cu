@@ -158,7 +158,9 @@ bool use_pair(const vsbp_bp *c, int l)
     // 1 (default): levels of >= pair_min_px pixels only -- a CTA walks its band row by row,
     // so small levels have too few CTAs to fill the GPU (levels 2-4 of C2 measured
     // 1.8-2.3x slower fused); 2: every level (tests)
-    return c->pair_fuse == 2 || (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px;
+    // u16-cost levels measured slower fused (C2 level 1 1.91 -> 2.05 ms, C4 level 1
+    // 0.193 -> 0.208 ms per pair): their staging doubles and the ring stays packed
+    return c->pair_fuse == 2 || (c->dbytes[l] == 1 && (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px);
 }
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
