@@ -223,11 +223,24 @@ __global__ void __launch_bounds__(CC_T) k_compact_write(const float *__restrict_
     }
     __syncthreads();
 
-    // ---- one contiguous, coalesced store of the tile's 3 * total floats
+    // ---- one contiguous, coalesced store of the tile's 3 * total floats: 8-byte
+    // stores (conflict-free LDS.64 from shared memory) after a one-float head that
+    // aligns the destination
     const long long base = tile_off[t];
     const long long lim = min((long long)total, a.cap - base);  // points beyond the capacity are dropped
     float *dst = xyz + 3 * base;
-    for (int e = tid; e < 3 * lim; e += CC_T) __stcs(dst + e, sOut[e]);
+    const int nf = lim > 0 ? (int)(3 * lim) : 0;
+    const int head = min(nf, (int)(((uintptr_t)dst >> 2) & 1));
+    if (tid < head) __stcs(dst, sOut[0]);
+    const int n2 = (nf - head) >> 1;
+    float2 *d2 = reinterpret_cast<float2 *>(dst + head);
+    if (head) {
+        for (int q = tid; q < n2; q += CC_T) __stcs(d2 + q, make_float2(sOut[1 + 2 * q], sOut[2 + 2 * q]));
+    } else {
+        const float2 *s2 = reinterpret_cast<const float2 *>(sOut);
+        for (int q = tid; q < n2; q += CC_T) __stcs(d2 + q, s2[q]);
+    }
+    if (tid == 0 && head + 2 * n2 < nf) __stcs(dst + nf - 1, sOut[nf - 1]);
 }
 
 int compact_tiles_per_pair(int W, int H) { return (W * H + CC_TILE - 1) / CC_TILE; }

@@ -120,15 +120,20 @@ def test_guard_rectify():
 
 
 # ----------------------------------------------------------------------------- a1-a5
-@pytest.mark.parametrize("W,H,L,levels,iters,msg_bytes,kernel,final", [
-    (45, 31, 64, 4, 5, 0, 0, 0), (45, 31, 64, 4, 5, 0, 0, 2), (37, 19, 48, 3, 4, 0, 0, 1),
-    (33, 17, 24, 3, 3, 2, 0, 0), (29, 13, 16, 2, 5, 4, 1, 0), (70, 9, 128, 5, 6, 0, 0, 0)])
-def test_guard_bp(W, H, L, levels, iters, msg_bytes, kernel, final):
+@pytest.mark.parametrize("W,H,L,levels,iters,msg_bytes,kernel,final,pair", [
+    (45, 31, 64, 4, 5, 0, 0, 0, 1), (45, 31, 64, 4, 5, 0, 0, 2, 1), (37, 19, 48, 3, 4, 0, 0, 1, 1),
+    (33, 17, 24, 3, 3, 2, 0, 0, 1), (29, 13, 16, 2, 5, 4, 1, 0, 1), (70, 9, 128, 5, 6, 0, 0, 0, 1),
+    (45, 31, 64, 4, 5, 0, 0, 0, 2), (133, 70, 64, 3, 7, 0, 0, 0, 2), (70, 9, 128, 5, 6, 0, 0, 0, 2),
+    (37, 19, 48, 3, 4, 0, 0, 0, 2)])
+def test_guard_bp(W, H, L, levels, iters, msg_bytes, kernel, final, pair):
+    """pair = 2: two iterations per launch on every level (cp.async staging, the
+    shared-memory ring, the second message array)."""
     rng = np.random.default_rng(W * L + final)
     B = 2
     left = rng.integers(0, 256, size=(B, H, W), dtype=np.uint8)
     right = rng.integers(0, 256, size=(B, H, W), dtype=np.uint8)
-    bp = P.StereoBP(W, H, L, levels, iters, batch=B, msg_bytes=msg_bytes, kernel=kernel, final=final, device="cuda")
+    bp = P.StereoBP(W, H, L, levels, iters, batch=B, msg_bytes=msg_bytes, kernel=kernel, final=final, device="cuda",
+                    pair=pair)
     nbytes = bp.workspace.numel()
 
     def setup(ar):
