@@ -79,8 +79,10 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        the grey images inside the message update, so D_0 is
  *                        neither stored nor read (bp_get_costs rebuilds it on demand
  *                        from the last call's images); 0 (default) = store and read
- *                        D_0.  Results are identical; 1 trades 11 % of the level-0
- *                        bytes for ~10 % more ALU work and measured slower. */
+ *                        D_0.  2 = only the one-iteration level-0 launches compute it
+ *                        (D_0 still stored for the two-iteration kernel).  Results
+ *                        are identical; both trade level-0 bytes for ALU work and
+ *                        measured slower. */
 #define VSBP_OPT_DIMG 3
 /*   VSBP_OPT_FINAL     : 1 or 2 = the last level-0 iteration is fused with the WTA
  *                        of both colours: its messages go straight into the

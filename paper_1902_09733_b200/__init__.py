@@ -159,8 +159,10 @@ class StereoBP:
             _check(lib().bp_set_option(self._h, VSBP_OPT_MSG_BYTES, msg_bytes), "bp_set_option")
         if kernel:
             _check(lib().bp_set_option(self._h, VSBP_OPT_KERNEL, kernel), "bp_set_option")
-        if dimg:
-            _check(lib().bp_set_option(self._h, VSBP_OPT_DIMG, 1), "bp_set_option")
+        if not dimg and os.environ.get("VSBP_DIMG"):  # experiment knob
+            dimg = int(os.environ["VSBP_DIMG"])
+        if dimg:  # 1: every level-0 update computes D_0 from the images; 2: one-iteration launches only
+            _check(lib().bp_set_option(self._h, VSBP_OPT_DIMG, int(dimg)), "bp_set_option")
         if final is None:  # experiment knob: VSBP_FINAL in the environment
             final = int(os.environ.get("VSBP_FINAL", "0"))
         if final:  # fused last level-0 iteration + WTA (level-0 messages not stored)

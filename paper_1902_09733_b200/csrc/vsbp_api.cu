@@ -140,6 +140,9 @@ bool use_fast(const vsbp_bp *c, int l)
 
 // level 0 of the packed kernel computes its data term from the grey images
 bool use_dimg(const vsbp_bp *c) { return c->dimg && use_fast(c, 0) && c->dbytes[0] == 1 && c->tau_d <= 255; }
+// VSBP_OPT_DIMG = 2: only the one-iteration level-0 launches compute the data term from
+// the images; D_0 is still stored for the two-iteration kernel
+bool dimg_only_singles(const vsbp_bp *c) { return use_dimg(c) && c->dimg == 2; }
 // k_final_fast: packed level-0 update with u8 costs read from memory, a normal
 // (MODE 0) last iteration, and a left neighbour for every colour-A pixel but x = 0
 bool use_final(const vsbp_bp *c)
@@ -154,7 +157,7 @@ bool use_final(const vsbp_bp *c)
 bool use_pair(const vsbp_bp *c, int l)
 {
     if (!c->pair_fuse || !use_fast(c, l) || c->iters < 3 || c->G > 32) return false;
-    if (l == 0 && use_dimg(c)) return false;
+    if (l == 0 && use_dimg(c) && !dimg_only_singles(c)) return false;
     // 1 (default): levels of >= pair_min_px pixels only -- a CTA walks its band row by row,
     // so small levels have too few CTAs to fill the GPU (levels 2-4 of C2 measured
     // 1.8-2.3x slower fused); 2: every level (tests)
@@ -333,7 +336,7 @@ int bp_set_option(vsbp_bp *c, int option, int value)
         return VSBP_OK;
     }
     if (option == VSBP_OPT_DIMG) {
-        if (value < 0 || value > 1) return VSBP_EINVAL;
+        if (value < 0 || value > 2) return VSBP_EINVAL;
         c->dimg = value;
         return VSBP_OK;
     }
@@ -449,7 +452,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         a.F = F;
         a.lam_q = c->lam_q;
         a.tau_d = c->tau_d;
-        a.write0 = use_dimg(c) ? 0 : 1;  // D_0 is never read when the update computes it
+        a.write0 = (use_dimg(c) && !dimg_only_singles(c)) ? 0 : 1;  // D_0 is never read when every update computes it
         CK(vsbp::launch_costpyr(left, right, a, B, st));
         l_from = F - 1;
     } else {
