@@ -85,17 +85,18 @@ struct JbuFastArgs {
 // the valid pixels of one row segment of a warp (lane: c pixels starting at raster
 // column x of row y), counted per compaction tile; a warp's segment (<= 128 px)
 // meets at most two tiles.  Warp-uniform call.
+// Lane 0 is inside whenever any lane is (x grows with the lane), the segment's second
+// tile is the next one (raster order), and a warp counts <= 256 pixels, so both counts
+// travel packed in one reduction (low / high 16 bits).
 __device__ __forceinline__ void count_row(const JbuFastArgs &a, int b, int Wh, int y, int x, int c, bool inside)
 {
-    const int tt = inside ? (int)(((long long)y * Wh + x) >> a.tile_shift) : INT_MAX;
+    const int tt = inside ? (int)(((long long)y * Wh + x) >> a.tile_shift) : -1;
     const int tA = __shfl_sync(FULL, tt, 0);
-    const int cA = __reduce_add_sync(FULL, tt == tA ? c : 0);
-    const int cB = __reduce_add_sync(FULL, (tt != tA && inside) ? c : 0);
-    const int tB = __reduce_max_sync(FULL, (tt != tA && inside) ? tt : -1);
-    if ((threadIdx.x & 31) == 0) {
-        int *base = a.tile_cnt + (size_t)b * a.tiles_per_pair;
-        if (cA) atomicAdd(base + tA, cA);
-        if (cB) atomicAdd(base + tB, cB);
+    const int sum = __reduce_add_sync(FULL, tt == tA ? c : (c << 16));
+    if ((threadIdx.x & 31) == 0 && tA >= 0) {
+        int *base = a.tile_cnt + (size_t)b * a.tiles_per_pair + tA;
+        if (sum & 0xFFFF) atomicAdd(base, sum & 0xFFFF);
+        if (sum >> 16) atomicAdd(base + 1, sum >> 16);
     }
 }
 
@@ -493,22 +494,35 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
             }
         if (far) {
             // some centre is far in colour: that pixel references its window minimum
+            // (the window is the same for the thread's NR x P pixels: one pass over the
+            // taps, each tap record read once, every pixel's minimum in parallel)
+            int m[NR][P];
 #pragma unroll
             for (int r = 0; r < NR; ++r)
 #pragma unroll
-                for (int k = 0; k < P; ++k) {
-                    if (ref[r][k] <= a.far_thr) continue;
+                for (int k = 0; k < P; ++k) m[r][k] = ref[r][k];
+#pragma unroll 1
+            for (int ty = 0; ty < T; ++ty) {
+                if (cy - R + ty < 0 || cy - R + ty >= a.H) continue;
 #pragma unroll
-                    for (int ty = 0; ty < T; ++ty) {
-                        if (cy - R + ty < 0 || cy - R + ty >= a.H) continue;
-                        for (int tx = 0; tx < T; ++tx) {
-                            const int qx = cx - R + tx;
-                            if (qx < 0 || qx >= a.W) continue;
-                            const unsigned adq = __vabsdiffu4(Ip[r][k], sT[e0 + ty * lw + tx].x);
-                            ref[r][k] = min(ref[r][k], (int)__dp4a(adq, adq, 0u));
+                for (int tx = 0; tx < T; ++tx) {
+                    const int qx = cx - R + tx;
+                    if (qx < 0 || qx >= a.W) continue;
+                    const unsigned tq = sT[e0 + ty * lw + tx].x;
+#pragma unroll
+                    for (int r = 0; r < NR; ++r)
+#pragma unroll
+                        for (int k = 0; k < P; ++k) {
+                            const unsigned adq = __vabsdiffu4(Ip[r][k], tq);
+                            m[r][k] = min(m[r][k], (int)__dp4a(adq, adq, 0u));
                         }
-                    }
                 }
+            }
+#pragma unroll
+            for (int r = 0; r < NR; ++r)
+#pragma unroll
+                for (int k = 0; k < P; ++k)
+                    if (ref[r][k] > a.far_thr) ref[r][k] = m[r][k];
         }
         unsigned acc[NR][P];
 #pragma unroll
