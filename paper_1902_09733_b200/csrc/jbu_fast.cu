@@ -60,7 +60,7 @@ namespace vsbp {
 // JB_RP: row passes per CTA of the vector kernel (one staged footprint serves
 // JB_RP x JB_Y rows; fewer redundantly staged halo rows per pixel)
 #ifndef JB_RP
-#define JB_RP 2
+#define JB_RP 16
 #endif
 constexpr int JB_X = 32, JB_Y = 8, JB_RMAX = 8, JB_SMAX = 16, JB_TMAX = 2 * JB_RMAX + 1;
 constexpr int JB_LW = JB_X + 2 * JB_RMAX + 1, JB_LH = JB_Y + 2 * JB_RMAX + 1;
