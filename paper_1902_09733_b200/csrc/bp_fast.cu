@@ -781,55 +781,58 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                              (d0 + j + 8 >= a.L ? (SIGNED ? 0x7FFF0000u : 0xFFFF0000u) : 0u);
 
     // enqueue the global inputs of step `ya` (A row ya, B row ya-1) into stage[buf]
+    // per-thread constants of the prefetch: the thread's colour-A index iA = I0-1+g and
+    // colour-B index iA+1 in every row; offsets relative to the row's colour-A chunk
+    const int iA = I0 - 1 + g;
+    const bool colA = iA >= 0 && lio, colB = g < NI && iA + 1 < a.Wc && lio;
+    const uint32_t rA0 = (uint32_t)iA * Lp + (uint32_t)d0;  // + ya * rowstep
+    const uint8_t *MoB = Mr + (size_t)(cB * 4u) * P;        // colour-B planes of iteration t-1
+    const TD *DA = Db + cA * P, *DB = Db + cB * P;
+
+    // enqueue the global inputs of step `ya` (A row ya, B row ya-1) into stage[buf]
     auto issue = [&](int ya, int buf) {
         uint4 *st = stage + (size_t)buf * NST * PAIR_T + tid;
-        {
-            const bool row = ya >= 0 && ya < a.H;
-            const int i = I0 - 1 + g;
-            const uint32_t o = (cA + (uint32_t)ya) & 1u;
-            const int x = 2 * i + (int)o;
-            const bool io = row && i >= 0 && x < a.W && lio;
-            const bool has[4] = {ya > 0, ya < a.H - 1, x > 0, x < a.W - 1};
-            const uint32_t r = io ? ((uint32_t)ya * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0 : 0u;
-            if (MODEA == 0) {
-                const uint8_t *Mo = Mr + (size_t)(cB * 4u) * P;
-                cp_async16(st + 0 * PAIR_T, Mo + (io && has[0] ? 1u * P + r - rowstep : 0u), io && has[0]);
-                cp_async16(st + 1 * PAIR_T, Mo + (io && has[1] ? r + rowstep : 0u), io && has[1]);
-                cp_async16(st + 2 * PAIR_T, Mo + (io && has[2] ? 3u * P + r + (o - 1u) * Lp : 0u), io && has[2]);
-                cp_async16(st + 3 * PAIR_T, Mo + (io && has[3] ? 2u * P + r + o * Lp : 0u), io && has[3]);
-            } else if (MODEA == 2) {
-                const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
-                const int X = x >> 1, Y = ya >> 1;
-                const int pyu = (ya - 1) >> 1, pyd = (ya + 1) >> 1, pxl = (x - 1) >> 1, pxr = (x + 1) >> 1;
-                const uint32_t Wcp = (uint32_t)a.Wcp;
+        const uint32_t o = (cA + (uint32_t)ya) & 1u;  // colour-A parity of row ya (= colour B's of row ya-1)
+        const int xA = 2 * iA + (int)o;
+        const bool okA = colA && (unsigned)ya < (unsigned)a.H && xA < a.W;
+        const uint32_t rA = rA0 + (uint32_t)ya * rowstep;
+        if (MODEA == 0) {
+            const bool v0 = okA && ya > 0, v1 = okA && ya < a.H - 1, v2 = okA && xA > 0, v3 = okA && xA < a.W - 1;
+            cp_async16(st + 0 * PAIR_T, MoB + (v0 ? P + rA - rowstep : 0u), v0);
+            cp_async16(st + 1 * PAIR_T, MoB + (v1 ? rA + rowstep : 0u), v1);
+            cp_async16(st + 2 * PAIR_T, MoB + (v2 ? 3u * P + rA + (o - 1u) * Lp : 0u), v2);
+            cp_async16(st + 3 * PAIR_T, MoB + (v3 ? 2u * P + rA + o * Lp : 0u), v3);
+        } else if (MODEA == 2) {
+            const bool has[4] = {ya > 0, ya < a.H - 1, xA > 0, xA < a.W - 1};
+            const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
+            const int X = xA >> 1, Y = ya >> 1;
+            const int pyu = (ya - 1) >> 1, pyd = (ya + 1) >> 1, pxl = (xA - 1) >> 1, pxr = (xA + 1) >> 1;
+            const uint32_t Wcp = (uint32_t)a.Wcp;
 #pragma unroll
-                for (int k = 0; k < 4; ++k) {
-                    const int px = k == 2 ? pxl : (k == 3 ? pxr : X);
-                    const int py = k == 0 ? pyu : (k == 1 ? pyd : Y);
-                    const int slot = k ^ 1;
-                    const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
-                    const bool v = io && has[k] && ph;
-                    const uint32_t off = v ? ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
-                                                 ((uint32_t)py * Wcp + (uint32_t)(px >> 1)) * Lp + (uint32_t)d0
-                                           : 0u;
-                    cp_async16(st + k * PAIR_T, Mpb + off, v);
-                }
+            for (int k = 0; k < 4; ++k) {
+                const int px = k == 2 ? pxl : (k == 3 ? pxr : X);
+                const int py = k == 0 ? pyu : (k == 1 ? pyd : Y);
+                const int slot = k ^ 1;
+                const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
+                const bool v = okA && has[k] && ph;
+                const uint32_t off = v ? ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
+                                             ((uint32_t)py * Wcp + (uint32_t)(px >> 1)) * Lp + (uint32_t)d0
+                                       : 0u;
+                cp_async16(st + k * PAIR_T, Mpb + off, v);
             }
-            const uint4 *dp = reinterpret_cast<const uint4 *>(Db + cA * P + r);
-#pragma unroll
-            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + w) * PAIR_T, dp + w, io);
         }
         {
-            const int yb = ya - 1;
-            const bool row = yb >= Y0 && yb < Y1;
-            const int i = I0 + g;
-            const uint32_t o = (cB + (uint32_t)yb) & 1u;
-            const int x = 2 * i + (int)o;
-            const bool io = row && g < NI && i < a.Wc && x < a.W && lio;
-            const uint32_t r = io ? ((uint32_t)yb * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0 : 0u;
-            const uint4 *dp = reinterpret_cast<const uint4 *>(Db + cB * P + r);
+            const uint4 *dp = reinterpret_cast<const uint4 *>(DA + (okA ? rA : 0u));
 #pragma unroll
-            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + DW + w) * PAIR_T, dp + w, io);
+            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + w) * PAIR_T, dp + w, okA);
+        }
+        {
+            // colour-B pixel iA+1 of row ya-1: x = xA + 2, chunk offset rA - rowstep + Lp
+            const int yb = ya - 1;
+            const bool okB = colB && yb >= Y0 && yb < Y1 && xA + 2 < a.W;
+            const uint4 *dp = reinterpret_cast<const uint4 *>(DB + (okB ? rA - rowstep + Lp : 0u));
+#pragma unroll
+            for (int w = 0; w < DW; ++w) cp_async16(st + (4 + DW + w) * PAIR_T, dp + w, okB);
         }
         cp_async_commit();
     };
@@ -843,10 +846,6 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
         const uint4 *st = stage + (size_t)(s & 1) * NST * PAIR_T + tid;
         // ---- A-phase: colour-A pixel index I0-1+g of row ya (incl. the halo pixels)
         if (ya >= 0 && ya < a.H) {
-            const int i = I0 - 1 + g;
-            const uint32_t o = (cA + (uint32_t)ya) & 1u;
-            const int x = 2 * i + (int)o;
-            const bool io = i >= 0 && x < a.W && lio;
             uint32_t dv[8], in[4][8];
 #pragma unroll
             for (int k = 0; k < 4; ++k) unpack_u8(MODEA == 1 ? make_uint4(0u, 0u, 0u, 0u) : st[k * PAIR_T], in[k]);
@@ -857,7 +856,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
-            (void)io;  // staged chunks of pixels outside the image are zero
+            // (staged chunks of pixels outside the image are zero)
             uint4 *const dst[4] = {ring0 + tid, ring1 + (size_t)((ya + 3) % 3) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 0) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 1) * RB + tid};
@@ -874,12 +873,11 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
         // ---- B-phase: colour-B pixel index I0+g of row yb = ya-1, from the ring
         const int yb = ya - 1;
         if (yb >= Y0 && yb < Y1) {  // block-uniform: every lane takes part in the group shuffles
-            const int i = I0 + g;
-            const uint32_t o = (cB + (uint32_t)yb) & 1u;
-            const int x = 2 * i + (int)o;
-            const bool io = g < NI && i < a.Wc && x < a.W && lio;
+            const uint32_t o = (cA + (uint32_t)ya) & 1u;  // colour-B parity of row yb
+            const int x = 2 * (iA + 1) + (int)o;
+            const bool io = colB && x < a.W;
             const bool has[4] = {yb > 0, yb < a.H - 1, x > 0, x < a.W - 1};
-            const uint32_t r = ((uint32_t)yb * (uint32_t)a.Wc + (uint32_t)i) * Lp + (uint32_t)d0;
+            const uint32_t r = rA0 + (uint32_t)yb * rowstep + Lp;
             // A(i, yb-1) sends down (slot 1), A(i, yb+1) up (slot 0), A(i-1+o, yb) right
             // (slot 3), A(i+o, yb) left (slot 2); the group of A index j is j - (I0 - 1)
             const uint4 *src[4] = {ring1 + (size_t)((yb + 2) % 3) * RB + (g + 1) * G + lane_g,
