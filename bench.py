@@ -384,8 +384,9 @@ def run_ours(args):
         all_bytes = sum(x["bytes"] for x in lv)
         all_ms = sum(x["ms"] for x in lv)
         roofline = {
-            "kernel": "level-0 message updates (a3+a4): k_update_pair (two iterations per launch) + k_update_fast "
-                      "(the last iteration)", "bound": "hbm", "achieved": achieved, "peak": peak,
+            "kernel": "level-0 message updates (a3+a4): k_update_pair (two iterations per launch; the last "
+                      "iteration fused with the WTA of both colours, a5)", "bound": "hbm", "achieved": achieved,
+            "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(B),
             "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
@@ -393,8 +394,9 @@ def run_ours(args):
             "share_of_step": all_ms / (ms if ms > 0 else 1.0),
             "all_levels_gbs": (all_bytes / 1e9) / (all_ms / 1e3) if all_ms > 0 else 0.0,
             "note": "bytes = the fused schedule's algorithmic bytes (a two-iteration launch moves 10L per pixel "
-                    "pair, 0.56x two one-iteration launches); k_update_pair is bound by the integer ALU pipe "
-                    "(ncu 83 %, 64 lane-ops/clk/SM measured by tools/micro/alu_bench), the last iteration by HBM",
+                    "pair, 0.56x two one-iteration launches; the fused last iteration + WTA moves D of both colours and "
+                    "one colour's 4 incoming messages, 6L per pixel pair); k_update_pair is bound by the integer "
+                    "ALU pipe (ncu 83 %, 64 lane-ops/clk/SM measured by tools/micro/alu_bench)",
         }
 
     # ---- CPU baseline: the oracle on this host's cores (rank 0 at N=1 only)

@@ -90,11 +90,14 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        bp_get_messages(level 0) returns VSBP_EINVAL after such a
  *                        call.  1: each colour-B pixel recomputes its neighbours'
  *                        messages (k_final_fast); 2: tiles keep the messages in
- *                        shared memory (k_final_tile).  0 (default) = store them and
- *                        label in separate passes.  Disparities are identical; both
- *                        fused variants move fewer bytes but measured slower
- *                        (DESIGN.md §12).  Applies when the packed kernels run with
- *                        u8 level-0 costs, iters >= 2 and W >= 2. */
+ *                        shared memory (k_final_tile); 3: the two-iteration
+ *                        kernel's row wavefront -- the A-phase updates and labels
+ *                        colour A, the B-phase labels colour B from the on-chip
+ *                        messages (the pipeline's setting).  0 (default) = store
+ *                        them and label in separate passes.  Disparities are
+ *                        identical; 1 and 2 measured slower.
+ *                        Applies when the packed kernels run with u8 level-0
+ *                        costs, iters >= 2 and W >= 2. */
 #define VSBP_OPT_FINAL 4
 /*   VSBP_OPT_PAIR      : 1 (default) = two checkerboard iterations per launch on
  *                        large levels where the packed kernel runs with

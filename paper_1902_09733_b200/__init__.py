@@ -581,8 +581,12 @@ class StereoPipeline:
             self.bp = ConstantSpaceBP(self.W, self.H, ndisp, levels, iters, csbp_k0, lam, data_trunc, disc_trunc,
                                       batch=batch, device=device)
         else:
+            # the pipeline never exports messages: the last level-0 iteration and both
+            # colours' WTA run as one row-wavefront launch (VSBP_OPT_FINAL = 3); the
+            # VSBP_FINAL environment knob still overrides it for experiments
+            final = int(os.environ.get("VSBP_FINAL", "3"))
             self.bp = StereoBP(self.W, self.H, ndisp, levels, iters, lam, data_trunc, disc_trunc, batch=batch,
-                               msg_bytes=msg_bytes, device=device)
+                               msg_bytes=msg_bytes, device=device, final=final)
         dev = torch.device(device)
         # 2B grey frames: [2][B] for independent pairs, the first B+1 for a frame run
         self.gray_flat = torch.empty((2 * batch, self.H, self.W), dtype=torch.uint8, device=dev)

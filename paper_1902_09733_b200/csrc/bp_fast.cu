@@ -741,7 +741,12 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // not exist), so the barrier-separated phases never wait on HBM latency:
 //   stage[buf][0..3][tid]   the 4 incoming chunks of the thread's colour-A pixel
 //   stage[buf][4..4+DW)     its D chunk(s);  stage[buf][4+DW..4+2DW)  the colour-B pixel's
-template <typename TD, int MODEA, bool PAD, bool SIGNED, int GT>
+// FIN: the level's LAST iteration (colour A, MODE 0) fused with the WTA (a5) of both
+// colours: the A-phase labels its pixels from the staged incoming (the belief is in
+// registers), keeps its outgoing messages in the ring, and the B-phase only labels the
+// colour-B pixels from them -- no message is written (bp_get_messages(level 0) is then
+// unavailable, as with VSBP_OPT_FINAL 1/2).  HBM per pixel pair: D_A + D_B + 4L.
+template <typename TD, int MODEA, bool PAD, bool SIGNED, int GT, bool FIN>
 __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD *__restrict__ D, int band)
 {
     const int G = GT ? GT : a.G, LOG2G = GT == 1 ? 0 : GT == 2 ? 1 : GT == 4 ? 2 : GT == 8 ? 3 : a.log2G;
@@ -857,6 +862,15 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
             // (staged chunks of pixels outside the image are zero)
+            if (FIN) {  // a5 for the colour-A pixel: D + its 4 incoming, ties -> smallest label
+                uint32_t tot[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) tot[j] = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+                const uint32_t lab = wta_key<PAD>(tot, d0, a.L, G);
+                const int xA = 2 * iA + (int)((cA + (uint32_t)ya) & 1u);
+                if (lane_g == 0 && colA && xA < a.W && g >= 1 && g <= NI && ya >= Y0 && ya < Y1)
+                    a.disp[((size_t)b * a.H + ya) * a.W + xA] = (int32_t)lab;
+            }
             uint4 *const dst[4] = {ring0 + tid, ring1 + (size_t)((ya + 3) % 3) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 0) * RB + tid,
                                    ring23 + (size_t)((ya & 1) * 2 + 1) * RB + tid};
@@ -904,10 +918,19 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
-            uint8_t *Mo = Mw + (size_t)(cB * 4u) * P + r;
-            outgoing<PAD, SIGNED, GT>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
-                if (io) *reinterpret_cast<uint4 *>(Mo + (size_t)k * P) = pack_u8(o8);
-            });
+            if (FIN) {  // a5 for the colour-B pixel from colour A's final messages
+                uint32_t tot[8];
+#pragma unroll
+                for (int j = 0; j < 8; ++j) tot[j] = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+                const uint32_t lab = wta_key<PAD>(tot, d0, a.L, G);
+                if (lane_g == 0 && io) a.disp[((size_t)b * a.H + yb) * a.W + x] = (int32_t)lab;
+                (void)r;
+            } else {
+                uint8_t *Mo = Mw + (size_t)(cB * 4u) * P + r;
+                outgoing<PAD, SIGNED, GT>(a, dv, in, padm, lane_g, [&](int k, const uint32_t o8[8]) {
+                    if (io) *reinterpret_cast<uint4 *>(Mo + (size_t)k * P) = pack_u8(o8);
+                });
+            }
         }
         __syncthreads();
     }
@@ -920,7 +943,7 @@ size_t pair_smem_bytes(int dbytes)
 }
 
 cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,
-                               cudaStream_t st)
+                               cudaStream_t st, bool fin)
 {
     const int NI = (PAIR_T >> a.log2G) - 2;
     dim3 grid((unsigned)((a.Wc + NI - 1) / NI), (unsigned)((a.H + band - 1) / band), (unsigned)B);
@@ -928,7 +951,7 @@ cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int
     const bool pad = (a.L % CH) != 0 || a.G != a.nch;
 #define VSBP_KG(TD_, MODE_, PAD_, SG_, GT_)                                                                     \
     do {                                                                                                        \
-        auto kf = k_update_pair<TD_, MODE_, PAD_, SG_, GT_>;                                                    \
+        auto kf = k_update_pair<TD_, MODE_, PAD_, SG_, GT_, false>;                                             \
         static cudaError_t attr = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
         if (attr != cudaSuccess) return attr;                                                                   \
         kf<<<grid, PAIR_T, smem, st>>>(a, (const TD_ *)D, band);                                                \
@@ -950,7 +973,25 @@ cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int
     case 1: VSBP_P(TD_, 1) break; \
     default: VSBP_P(TD_, 2) break; \
     }
-    if (dbytes == 1) {
+    if (fin) {
+        // the final iteration + WTA: u8 costs, MODE 0 only (use_final)
+        if (dbytes != 1 || mode != 0) return cudaErrorInvalidValue;
+#define VSBP_F(PAD_, SG_, GT_)                                                                                  \
+    do {                                                                                                        \
+        auto kf = k_update_pair<uint8_t, 0, PAD_, SG_, GT_, true>;                                              \
+        static cudaError_t attr = cudaFuncSetAttribute(kf, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem); \
+        if (attr != cudaSuccess) return attr;                                                                   \
+        kf<<<grid, PAIR_T, smem, st>>>(a, (const uint8_t *)D, band);                                            \
+    } while (0)
+        if (!pad && a.G == 4) {
+            if (sgn) VSBP_F(false, true, 4); else VSBP_F(false, false, 4);
+        } else if (pad) {
+            if (sgn) VSBP_F(true, true, 0); else VSBP_F(true, false, 0);
+        } else {
+            if (sgn) VSBP_F(false, true, 0); else VSBP_F(false, false, 0);
+        }
+#undef VSBP_F
+    } else if (dbytes == 1) {
         VSBP_M(uint8_t)
     } else {
         VSBP_M(uint16_t)

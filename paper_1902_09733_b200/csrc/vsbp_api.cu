@@ -147,7 +147,8 @@ bool dimg_only_singles(const vsbp_bp *c) { return use_dimg(c) && c->dimg == 2; }
 // (MODE 0) last iteration, and a left neighbour for every colour-A pixel but x = 0
 bool use_final(const vsbp_bp *c)
 {
-    return c->final_fuse && use_fast(c, 0) && !use_dimg(c) && c->dbytes[0] == 1 && c->iters >= 2 && c->W >= 2;
+    return c->final_fuse && use_fast(c, 0) && !use_dimg(c) && c->dbytes[0] == 1 && c->iters >= 2 && c->W >= 2 &&
+           (c->final_fuse != 3 || c->G <= 32);
 }
 
 // two iterations per launch (k_update_pair): the packed kernel with D from memory,
@@ -341,7 +342,7 @@ int bp_set_option(vsbp_bp *c, int option, int value)
         return VSBP_OK;
     }
     if (option == VSBP_OPT_FINAL) {
-        if (value < 0 || value > 2) return VSBP_EINVAL;
+        if (value < 0 || value > 3) return VSBP_EINVAL;
         c->final_fuse = value;
         return VSBP_OK;
     }
@@ -520,7 +521,9 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 const bool wta = (l == 0 && t == c->iters - 1);  // a5 fused for this colour
                 if (wta && use_final(c)) {
                     // last iteration + WTA of both colours, messages not stored
-                    if (c->final_fuse == 2)
+                    if (c->final_fuse == 3)  // row wavefront: A labelled with its update, B from the ring
+                        CK(vsbp::launch_update_pair(D, 1, fa, B, 0, fast_signed(c, l), c->pair_band, st, true));
+                    else if (c->final_fuse == 2)
                         CK(vsbp::launch_final_tile(D, fa, B, fast_signed(c, l), st));
                     else
                         CK(vsbp::launch_final_fast(D, fa, B, fast_signed(c, l), st));

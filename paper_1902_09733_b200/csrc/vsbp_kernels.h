@@ -61,7 +61,7 @@ cudaError_t launch_update_fast(const void *D, int dbytes, const FastArgs &a, int
 // a.M (or the parent, mode 2; nothing, mode 1) and writing the second colour's
 // messages to a.Mw; rows per CTA band
 cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,
-                               cudaStream_t st);
+                               cudaStream_t st, bool fin = false);
 size_t pair_smem_bytes(int dbytes);
 // fused last level-0 iteration + WTA of both colours (a.colour = the colour updated last)
 cudaError_t launch_final_fast(const void *D, const FastArgs &a, int B, bool sgn, cudaStream_t st);

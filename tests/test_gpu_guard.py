@@ -124,7 +124,7 @@ def test_guard_rectify():
     (45, 31, 64, 4, 5, 0, 0, 0, 1), (45, 31, 64, 4, 5, 0, 0, 2, 1), (37, 19, 48, 3, 4, 0, 0, 1, 1),
     (33, 17, 24, 3, 3, 2, 0, 0, 1), (29, 13, 16, 2, 5, 4, 1, 0, 1), (70, 9, 128, 5, 6, 0, 0, 0, 1),
     (45, 31, 64, 4, 5, 0, 0, 0, 2), (133, 70, 64, 3, 7, 0, 0, 0, 2), (70, 9, 128, 5, 6, 0, 0, 0, 2),
-    (37, 19, 48, 3, 4, 0, 0, 0, 2)])
+    (37, 19, 48, 3, 4, 0, 0, 0, 2), (133, 70, 64, 3, 5, 0, 0, 3, 2), (37, 19, 48, 3, 4, 0, 0, 3, 2)])
 def test_guard_bp(W, H, L, levels, iters, msg_bytes, kernel, final, pair):
     """pair = 2: two iterations per launch on every level (cp.async staging, the
     shared-memory ring, the second message array)."""

@@ -45,7 +45,7 @@ def check_bp_case(left, right, L, levels, iters, lam=0.07, dt=15.0, st=1.7, msg_
     d_o, msgs_o = oracle.bp_disparity(left, right, L, levels, iters, lam, dt, st, return_messages=True)
     _, disp_1 = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, pair=0)
     assert np.array_equal(disp_1[0], d_o), "disparity differs (one iteration per launch)"
-    for variant in (1, 2):
+    for variant in (1, 2, 3):
         _, disp_f = run_gpu_bp(left, right, L, levels, iters, lam, dt, st, msg_bytes, final=variant)
         assert np.array_equal(disp_f[0], d_o), f"disparity differs (fused final iteration, variant {variant})"
     assert np.array_equal(disp[0], d_o), "disparity differs"
@@ -786,7 +786,7 @@ def test_config4_pipeline_jbu_s2_r3():
 @pytest.mark.parametrize("W,H,L,levels,iters", [(2, 1, 16, 1, 2), (3, 5, 16, 1, 3), (2, 9, 48, 2, 4), (17, 1, 32, 1, 5),
                                                 (31, 23, 48, 3, 2), (64, 48, 64, 4, 5), (65, 33, 128, 5, 6),
                                                 (40, 31, 64, 3, 8)])
-@pytest.mark.parametrize("variant", [1, 2])
+@pytest.mark.parametrize("variant", [1, 2, 3])
 def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters, variant):
     """VSBP_OPT_FINAL=1: the last level-0 iteration's messages go straight
     into the receivers' beliefs.  Disparities equal the oracle and the stored-message
@@ -796,9 +796,9 @@ def test_fused_final_iteration_matches_oracle(W, H, L, levels, iters, variant):
     l = rng.integers(0, 256, size=(2, H, W), dtype=np.uint8)
     r = np.roll(l, 3, axis=2)
     r = np.clip(r.astype(np.int32) + rng.integers(-6, 7, size=r.shape), 0, 255).astype(np.uint8)
-    bp = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=variant)
+    bp = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=variant, pair=2)
     disp = bp.disparity(to_dev(l), to_dev(r)).cpu().numpy()
-    ref = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=0).disparity(to_dev(l), to_dev(r))
+    ref = P.StereoBP(W, H, L, levels, iters, batch=2, device=dev(), final=0, pair=0).disparity(to_dev(l), to_dev(r))
     assert np.array_equal(disp, ref.cpu().numpy())
     for b in range(2):
         assert np.array_equal(disp[b], oracle.bp_disparity(l[b], r[b], L, levels, iters))

@@ -3,8 +3,8 @@
 #   tools/final_round.sh TAG
 # 1) all GPU tests, 2) smoke(), 3) the default bench line (N=1, cpu_baseline, e2e),
 # 4) the reference (oracle) arm, 5) f-row timings, 6) the ncu launch list of the
-# bench command and one --set full capture each of the two-iteration and single
-# level-0 updates, the JBU and the compaction write.  Every step runs without ncu
+# bench command and one --set full capture each of the two-iteration and final
+# (last iteration + WTA) level-0 updates, the JBU and the compaction write.  Every step runs without ncu
 # first.  Outputs in gpurun_out/.
 TAG=${1:-final}
 mkdir -p gpurun_out
@@ -17,9 +17,10 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 256"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
-for cap in ${CAPS:-k_update_pair:3 k_update_fast:8 k_jbu_vec:1 k_compact_write:1}; do
+# k_update_pair launches per step: two fused pairs, then the last iteration + WTA (FIN)
+for cap in ${CAPS:-k_update_pair:3 k_update_pair:5 k_jbu_vec:1 k_compact_write:1}; do
     K=${cap%%:*}; S=${cap##*:}
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
-        -o gpurun_out/prof_${TAG}_$K python bench.py $ARGS > gpurun_out/ncu_full_${TAG}_$K.log 2>&1
-    echo "full $K rc=$?"
+        -o gpurun_out/prof_${TAG}_${K}_s$S python bench.py $ARGS > gpurun_out/ncu_full_${TAG}_${K}_s$S.log 2>&1
+    echo "full $K (skip $S) rc=$?"
 done
