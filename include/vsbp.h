@@ -84,7 +84,7 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        are identical; both trade level-0 bytes for ALU work and
  *                        measured slower. */
 #define VSBP_OPT_DIMG 3
-/*   VSBP_OPT_FINAL     : 1 or 2 = the last level-0 iteration is fused with the WTA
+/*   VSBP_OPT_FINAL     : 1, 2 or 3 = the last level-0 iteration is fused with the WTA
  *                        of both colours: its messages go straight into the
  *                        receivers' beliefs and are never stored, so
  *                        bp_get_messages(level 0) returns VSBP_EINVAL after such a
@@ -97,7 +97,8 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        them and label in separate passes.  Disparities are
  *                        identical; 1 and 2 measured slower.
  *                        Applies when the packed kernels run with u8 level-0
- *                        costs, iters >= 2 and W >= 2. */
+ *                        costs, iters >= 2 and W >= 2 (3: also L <= 32 * 16,
+ *                        i.e. lane groups of at most 32). */
 #define VSBP_OPT_FINAL 4
 /*   VSBP_OPT_PAIR      : 1 (default) = two checkerboard iterations per launch on
  *                        large levels where the packed kernel runs with

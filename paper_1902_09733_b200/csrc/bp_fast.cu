@@ -139,6 +139,30 @@ __device__ __forceinline__ uint32_t chunk_min(const uint32_t h[8])
     return __vminu2(d, prmt(d, 0u, 0x1032));
 }
 
+// min over the 16 labels of two chunks: h0's in the low half, h1's in the high half
+__device__ __forceinline__ uint32_t chunk_min2(const uint32_t h0[8], const uint32_t h1[8])
+{
+    const uint32_t a0 = __vimin3_u16x2(__vimin3_u16x2(h0[0], h0[1], h0[2]), __vimin3_u16x2(h0[3], h0[4], h0[5]),
+                                       __vminu2(h0[6], h0[7]));
+    const uint32_t a1 = __vimin3_u16x2(__vimin3_u16x2(h1[0], h1[1], h1[2]), __vimin3_u16x2(h1[3], h1[4], h1[5]),
+                                       __vminu2(h1[6], h1[7]));
+    return __vminu2(prmt(a0, a1, 0x5410), prmt(a0, a1, 0x7632));
+}
+
+// The 3-tap truncated-linear envelope of a normalised chunk h (every half <= TT):
+// out_j = min(h_j, h_{j-1} + S, h_{j+1} + S).  h + S is formed with a plain 32-bit add
+// (no carry between the halves: TT + S < 2^16), which the compiler may put on the FMA
+// pipe, then one 3-input u16x2 min per word on the ALU pipe -- instead of two
+// add-min (VIADDMNMX) ALU instructions per word.  The lane-boundary neighbours `pv0`
+// (label d0-1, in the half matching e) and `nx7` (d0+16) arrive already offset by S.
+__device__ __forceinline__ void envelope(const uint32_t h[8], const uint32_t hs[8], uint32_t prev0s,
+                                         uint32_t next7s, uint32_t out[8])
+{
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+        out[j] = __vimin3_u16x2(h[j], j == 0 ? prev0s : hs[j - 1], j == 7 ? next7s : hs[j + 1]);
+}
+
 // MODE 0: normal iteration; 1: top level t=0 (all incoming 0); 2: lower level t=0
 // (incoming read from the parent level); 3: WTA only (no message update).
 // PAD: some labels of the chunk are >= L.  WTA: write the WTA label of the pixel.
@@ -248,9 +272,10 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
             }
         }
         // min over the G lanes: direction kp in the low half, kp+1 in the high half
-        uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
+        uint32_t pm = chunk_min2(h[0], h[1]);
         for (int s = a.G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, a.G));
-        // h' = min(h - min h, tau_q)
+        // h' = min(h - min h, tau_q), and h' + S for the envelope
+        uint32_t hs[2][8];
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
@@ -262,23 +287,22 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
 #pragma unroll
                 for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
             }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hs[e][j] = h[e][j] + a.SS;
         }
-        // labels d0-1 (lane-1's r7 high half) and d0+16 (lane+1's r0 low half)
-        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, a.G);
-        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, a.G);
+        // labels d0-1 (lane-1's r7 high half) and d0+16 (lane+1's r0 low half), + S
+        uint32_t up = __shfl_up_sync(FULL, prmt(hs[0][7], hs[1][7], 0x7632), 1, a.G);
+        uint32_t dn = __shfl_down_sync(FULL, prmt(hs[0][0], hs[1][0], 0x5410), 1, a.G);
         if (lane_g == 0) up = a.TT;
         if (lane_g == a.G - 1) dn = a.TT;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);  // (d0-1, d0+7)
-            const uint32_t next7 = prmt(h[e][0], dn, e == 0 ? 0x5432 : 0x7632);  // (d0+8, d0+16)
             uint32_t out[8];
+            envelope(h[e], hs[e], prmt(up, hs[e][7], e == 0 ? 0x5410 : 0x5432),  // (d0-1, d0+7)
+                     prmt(hs[e][0], dn, e == 0 ? 0x5432 : 0x7632), out);          // (d0+8, d0+16)
+            if (PAD) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t pv = j == 0 ? prev0 : h[e][j - 1];
-                const uint32_t nx = j == 7 ? next7 : h[e][j + 1];
-                out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[e][j]));
-                if (PAD) out[j] &= ~padm[j];
+                for (int j = 0; j < 8; ++j) out[j] &= ~padm[j];
             }
             if (io)
                 *reinterpret_cast<uint4 *>(Mb + ((a.colour * 4u + (uint32_t)(kp + e)) * P + r)) = pack_u8(out);
@@ -679,9 +703,10 @@ __device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8]
                 h[1][j] |= padm[j];
             }
         }
-        uint32_t pm = prmt(chunk_min(h[0]), chunk_min(h[1]), 0x5410);
+        uint32_t pm = chunk_min2(h[0], h[1]);
 #pragma unroll
         for (int s = G >> 1; s > 0; s >>= 1) pm = __vminu2(pm, __shfl_xor_sync(FULL, pm, s, G));
+        uint32_t hs[2][8];  // h' + S
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
             const uint32_t hm = prmt(pm, 0u, e == 0 ? 0x1010 : 0x3232);
@@ -693,22 +718,23 @@ __device__ __forceinline__ void outgoing(const FastArgs &a, const uint32_t dv[8]
 #pragma unroll
                 for (int j = 0; j < 8; ++j) h[e][j] = __vminu2(h[e][j] - hm, a.TT);
             }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) hs[e][j] = h[e][j] + a.SS;
         }
-        uint32_t up = __shfl_up_sync(FULL, prmt(h[0][7], h[1][7], 0x7632), 1, G);
-        uint32_t dn = __shfl_down_sync(FULL, prmt(h[0][0], h[1][0], 0x5410), 1, G);
+        // labels d0-1 (lane-1's r7 high half) and d0+16 (lane+1's r0 low half), + S;
+        // outside the chunk range TT (>= every h', so no effect)
+        uint32_t up = __shfl_up_sync(FULL, prmt(hs[0][7], hs[1][7], 0x7632), 1, G);
+        uint32_t dn = __shfl_down_sync(FULL, prmt(hs[0][0], hs[1][0], 0x5410), 1, G);
         if (lane_g == 0) up = a.TT;
         if (lane_g == G - 1) dn = a.TT;
 #pragma unroll
         for (int e = 0; e < 2; ++e) {
-            const uint32_t prev0 = prmt(up, h[e][7], e == 0 ? 0x5410 : 0x5432);
-            const uint32_t next7 = prmt(h[e][0], dn, e == 0 ? 0x5432 : 0x7632);
             uint32_t out[8];
+            envelope(h[e], hs[e], prmt(up, hs[e][7], e == 0 ? 0x5410 : 0x5432),
+                     prmt(hs[e][0], dn, e == 0 ? 0x5432 : 0x7632), out);
+            if (PAD) {
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-                const uint32_t pv = j == 0 ? prev0 : h[e][j - 1];
-                const uint32_t nx = j == 7 ? next7 : h[e][j + 1];
-                out[j] = __viaddmin_u16x2(pv, a.SS, __viaddmin_u16x2(nx, a.SS, h[e][j]));
-                if (PAD) out[j] &= ~padm[j];
+                for (int j = 0; j < 8; ++j) out[j] &= ~padm[j];
             }
             store(kp + e, out);
         }
