@@ -163,6 +163,29 @@ __device__ __forceinline__ void envelope(const uint32_t h[8], const uint32_t hs[
         out[j] = __vimin3_u16x2(h[j], j == 0 ? prev0s : hs[j - 1], j == 7 ? next7s : hs[j + 1]);
 }
 
+// WTA (a5) from the five belief terms of a chunk when every belief is below 2^12
+// (u8 costs: D + 4 tau_q <= 255 + 4 * 255): each u16 half becomes cost * 16 + its label
+// offset in the chunk (j, or j + 8 in the high half), formed by one multiply-add, so a
+// u16x2 min tree finds the minimum cost with the smallest label among equal costs;
+// the lanes then reduce (cost << 9 | label) keys.  Same result as wta_key.
+template <bool PAD>
+__device__ __forceinline__ uint32_t wta_key16(const uint32_t dv[8], const uint32_t (&in)[4][8], int d0, int L, int G)
+{
+    uint32_t k[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+        const uint32_t tot = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
+        k[j] = tot * 16u + ((uint32_t)j | ((uint32_t)(j + 8) << 16));  // no carry between halves
+        if (PAD) k[j] |= (d0 + j >= L ? 0x0000FFFFu : 0u) | (d0 + j + 8 >= L ? 0xFFFF0000u : 0u);
+    }
+    const uint32_t m = __vimin3_u16x2(__vimin3_u16x2(k[0], k[1], k[2]), __vimin3_u16x2(k[3], k[4], k[5]),
+                                      __vminu2(k[6], k[7]));
+    const uint32_t k16 = min(m & 0xFFFFu, m >> 16);  // low-half labels are the smaller ones
+    uint32_t best = ((k16 >> 4) << 9) | (uint32_t)d0 | (k16 & 15u);
+    for (int s = G >> 1; s > 0; s >>= 1) best = min(best, __shfl_xor_sync(FULL, best, s, G));
+    return best & 511u;
+}
+
 // MODE 0: normal iteration; 1: top level t=0 (all incoming 0); 2: lower level t=0
 // (incoming read from the parent level); 3: WTA only (no message update).
 // PAD: some labels of the chunk are >= L.  WTA: write the WTA label of the pixel.
@@ -234,7 +257,10 @@ __global__ void __launch_bounds__(256, 4) k_update_fast(FastArgs a, const TD *__
     for (int k = 0; k < 4; ++k) unpack_u8(wi[k], in[k]);
 
     // ---- fused WTA (a5): argmin of the belief D + sum of the 4 incoming, ties -> smallest d
-    if (WTA) {
+    if (WTA && sizeof(TD) == 1) {  // u8 costs (or the image data term, <= 255): beliefs < 2^12
+        const uint32_t lab = wta_key16<PAD>(dv, in, d0, a.L, a.G);
+        if (active && lane_g == 0) a.disp[((size_t)b * a.H + y) * a.W + x] = (int32_t)lab;
+    } else if (WTA) {
         uint32_t best = 0xFFFFFFFFu;
 #pragma unroll
         for (int j = 0; j < 8; ++j) {
@@ -889,10 +915,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
             }
             // (staged chunks of pixels outside the image are zero)
             if (FIN) {  // a5 for the colour-A pixel: D + its 4 incoming, ties -> smallest label
-                uint32_t tot[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) tot[j] = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
-                const uint32_t lab = wta_key<PAD>(tot, d0, a.L, G);
+                const uint32_t lab = wta_key16<PAD>(dv, in, d0, a.L, G);
                 const int xA = 2 * iA + (int)((cA + (uint32_t)ya) & 1u);
                 if (lane_g == 0 && colA && xA < a.W && g >= 1 && g <= NI && ya >= Y0 && ya < Y1)
                     a.disp[((size_t)b * a.H + ya) * a.W + xA] = (int32_t)lab;
@@ -945,10 +968,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
             if (FIN) {  // a5 for the colour-B pixel from colour A's final messages
-                uint32_t tot[8];
-#pragma unroll
-                for (int j = 0; j < 8; ++j) tot[j] = iadd3(dv[j], in[0][j], in[1][j]) + in[2][j] + in[3][j];
-                const uint32_t lab = wta_key<PAD>(tot, d0, a.L, G);
+                const uint32_t lab = wta_key16<PAD>(dv, in, d0, a.L, G);
                 if (lane_g == 0 && io) a.disp[((size_t)b * a.H + yb) * a.W + x] = (int32_t)lab;
                 (void)r;
             } else {
