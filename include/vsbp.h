@@ -109,8 +109,8 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        VSBP_OPT_PAIR_MINPX pixels).  The level's messages then
  *                        alternate between two arrays (bp_workspace_bytes grows by
  *                        one message array per such level).  2 = on every eligible
- *                        level (tests); 0 = one iteration per launch.  Results are
- *                        identical.
+ *                        level (tests); 3 = as 1 with u16-cost levels included;
+ *                        0 = one iteration per launch.  Results are identical.
  *   VSBP_OPT_PAIR_BAND : rows per CTA of the two-iteration kernel (default 64).
  *   VSBP_OPT_PAIR_MINPX: smallest level (W_l * H_l pixels) fused under
  *                        VSBP_OPT_PAIR = 1 (default 100000). */

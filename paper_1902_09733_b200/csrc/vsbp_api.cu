@@ -164,7 +164,9 @@ bool use_pair(const vsbp_bp *c, int l)
     // 1.8-2.3x slower fused); 2: every level (tests)
     // u16-cost levels measured slower fused (C2 level 1 1.91 -> 2.05 ms, C4 level 1
     // 0.193 -> 0.208 ms per pair): their staging doubles and the ring stays packed
-    return c->pair_fuse == 2 || (c->dbytes[l] == 1 && (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px);
+    // 3: as 1, u16-cost levels included
+    return c->pair_fuse == 2 ||
+           ((c->dbytes[l] == 1 || c->pair_fuse == 3) && (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px);
 }
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
@@ -347,7 +349,7 @@ int bp_set_option(vsbp_bp *c, int option, int value)
         return VSBP_OK;
     }
     if (option == VSBP_OPT_PAIR) {
-        if (value < 0 || value > 2) return VSBP_EINVAL;
+        if (value < 0 || value > 3) return VSBP_EINVAL;
         c->pair_fuse = value;
         c->ws = nullptr;  // plan changes (second message arrays): workspace must be re-bound
         c->ws_batch = 0;

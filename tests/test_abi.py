@@ -90,7 +90,7 @@ def test_level_dims_and_workspace():
     assert L.bp_workspace_bytes(h, 1) > n1
     assert L.bp_set_option(h, P.VSBP_OPT_MSG_BYTES, 3) == -1
     # 0/1 switches; anything else (or an unknown option) is refused
-    for opt, top in ((P.VSBP_OPT_KERNEL, 1), (P.VSBP_OPT_DIMG, 2), (P.VSBP_OPT_FINAL, 3), (P.VSBP_OPT_PAIR, 2)):
+    for opt, top in ((P.VSBP_OPT_KERNEL, 1), (P.VSBP_OPT_DIMG, 2), (P.VSBP_OPT_FINAL, 3), (P.VSBP_OPT_PAIR, 3)):
         assert all(L.bp_set_option(h, opt, v) == 0 for v in range(top + 1))
         assert L.bp_set_option(h, opt, top + 1) == -1 and L.bp_set_option(h, opt, -1) == -1
     assert L.bp_set_option(h, 99, 0) == -1
