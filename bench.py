@@ -166,6 +166,19 @@ def q_intrinsics():
     return I
 
 
+def ncu_pipes(batch: int):
+    """ncu pipe utilisation (% of peak sustained) of the captured level-0 update
+    launches (profiles/traffic.json, same command and batch), or None"""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            d = json.load(f)
+    except (OSError, ValueError):
+        return None
+    if int(d.get("batch", -1)) != batch:
+        return None
+    return {k: v for k, v in (d.get("pipes_pct") or {}).items() if k.startswith("k_update_pair")} or None
+
+
 def ncu_traffic(batch: int):
     """dram__bytes_read.sum + dram__bytes_write.sum per level-0 message-update launch
     (mean over the fused two-iteration and the one-iteration launches of an ncu launch
@@ -389,14 +402,17 @@ def run_ours(args):
             "peak": peak,
             "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
             "traffic": ncu_traffic(B),
+            # what binds it instead of HBM: the integer ALU pipe (ncu, same command)
+            "pipes_pct_ncu": ncu_pipes(B),
             "bytes_per_launch": l0["bytes"] / max(l0["launches"], 1),
             "us_per_launch": 1000.0 * l0["ms"] / max(l0["launches"], 1),
             "share_of_step": all_ms / (ms if ms > 0 else 1.0),
             "all_levels_gbs": (all_bytes / 1e9) / (all_ms / 1e3) if all_ms > 0 else 0.0,
             "note": "bytes = the fused schedule's algorithmic bytes (a two-iteration launch moves 10L per pixel "
                     "pair, 0.56x two one-iteration launches; the fused last iteration + WTA moves D of both colours and "
-                    "one colour's 4 incoming messages, 6L per pixel pair); k_update_pair is bound by the integer "
-                    "ALU pipe (ncu 83 %, 64 lane-ops/clk/SM measured by tools/micro/alu_bench)",
+                    "one colour's 4 incoming messages, 6L per pixel pair). Fusion trades HBM bytes for on-chip "
+                    "work: k_update_pair is bound by the integer ALU pipe (pipes_pct_ncu; the pipe runs 64 "
+                    "lane-ops/clk/SM, tools/micro/alu_bench), so its HBM fraction is not its binding roofline",
         }
 
     # ---- CPU baseline: the oracle on this host's cores (rank 0 at N=1 only)

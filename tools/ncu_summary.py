@@ -119,6 +119,25 @@ def rep_traffic(path):
     return res
 
 
+def rep_pipes(path):
+    """{short kernel name: {pipe: % of peak sustained active}} for the ALU, FMA and XU
+    pipes and the issue slots (what binds a kernel that is not HBM-bound)"""
+    out = subprocess.run(["ncu", "-i", path, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(out)))
+    if len(rows) < 3:
+        return {}
+    h = rows[0]
+    ms = {"alu": "sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active",
+          "fma": "sm__inst_executed_pipe_fma.avg.pct_of_peak_sustained_active",
+          "xu": "sm__inst_executed_pipe_xu.avg.pct_of_peak_sustained_active",
+          "issue": "smsp__issue_active.avg.pct_of_peak_sustained_active"}
+    res = {}
+    for rr in rows[2:]:
+        name = rr[h.index("Kernel Name")].split("(")[0].replace("void ", "")
+        res[name] = {k: round(float(rr[h.index(m)].replace(",", "")), 1) for k, m in ms.items() if m in h}
+    return res
+
+
 def level0_traffic(path):
     """Mean DRAM bytes (read + write) per level-0 message-update launch -- the fused
     two-iteration launches (k_update_pair with u8 costs) and the one-iteration updates
@@ -159,11 +178,12 @@ def main():
         parts.append("## Launch list (ncu `gpu__time_duration.sum`, cold-cache, serialised)\n")
         parts.append(f"Total device time of the captured launches: {tot:.1f} us\n")
         parts.append(t + "\n")
-    traffic = {}
+    traffic, pipes = {}, {}
     for rep in a.rep:
         parts.append("## `--set full` capture\n")
         parts.append(rep_metrics(rep) + "\n")
         traffic.update(rep_traffic(rep))
+        pipes.update(rep_pipes(rep))
     if a.traffic_json:
         import json
         level0 = level0_traffic(a.launches) if a.launches else None
@@ -171,7 +191,7 @@ def main():
             # bench.py reports the level-0 message updates' traffic (its roofline kernels):
             # the mean DRAM bytes per level-0 update launch over the launch list
             json.dump({"batch": a.batch, "source": a.out, "dram_bytes_per_launch": traffic,
-                       "level0_update": level0}, f, indent=1)
+                       "pipes_pct": pipes, "level0_update": level0}, f, indent=1)
     with open(a.out, "w") as f:
         f.write("\n".join(parts))
     print(open(a.out).read())
