@@ -778,7 +778,20 @@ __device__ __forceinline__ void load_d(const TD *p, bool io, uint32_t dv[8])
     }
 }
 
-constexpr int PAIR_T = 256;  // threads per CTA of k_update_pair
+// CTA size and staging depth of k_update_pair: 128 threads with one
+// staging buffer take 44 KB of shared memory (u8 costs), so 5 CTAs (20 warps) fit an
+// SM; 256 threads with double buffering (112 KB, 16 warps) measured 10 % slower
+#ifndef VSBP_PAIR_T
+#define VSBP_PAIR_T 128
+#endif
+#ifndef VSBP_PAIR_NBUF
+#define VSBP_PAIR_NBUF 1
+#endif
+constexpr int PAIR_T = VSBP_PAIR_T;  // threads per CTA of k_update_pair
+// staging buffers: 2 = cp.async into the other buffer while this step reads its own;
+// 1 = the step first moves its staged inputs to registers, then refills the buffer
+constexpr int PAIR_NBUF = VSBP_PAIR_NBUF;
+constexpr int PAIR_MINB = PAIR_T == 256 ? 2 : (PAIR_NBUF == 1 ? 5 : 4);
 
 __device__ __forceinline__ void cp_async16(void *sdst, const void *gsrc, bool valid)
 {
@@ -799,7 +812,7 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 // colour-B pixels from them -- no message is written (bp_get_messages(level 0) is then
 // unavailable, as with VSBP_OPT_FINAL 1/2).  HBM per pixel pair: D_A + D_B + 4L.
 template <typename TD, int MODEA, bool PAD, bool SIGNED, int GT, bool FIN>
-__global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD *__restrict__ D, int band)
+__global__ void __launch_bounds__(PAIR_T, PAIR_MINB) k_update_pair(FastArgs a, const TD *__restrict__ D, int band)
 {
     const int G = GT ? GT : a.G, LOG2G = GT == 1 ? 0 : GT == 2 ? 1 : GT == 4 ? 2 : GT == 8 ? 3 : a.log2G;
     constexpr int DW = sizeof(TD) == 1 ? 1 : 2;  // 16-byte D chunks per lane
@@ -809,13 +822,13 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
     // A-phase, no unpack in the B-phase), one buffer per (slot, row) still to be read:
     // slot 0 of row ya (read by B(ya-1) in the same step), slots 2/3 of rows ya and
     // ya-1 (B(ya-1), B(ya)), slot 1 of rows ya-2..ya (B(ya-1), B(ya), B(ya+1))
-    // (u16 costs need 2x the staging, so their ring stays packed u8: 2 CTAs per SM either way)
+    // (u16 costs need 2x the staging, so their ring stays packed u8)
     constexpr bool UNPK = sizeof(TD) == 1;
     constexpr int RB = (UNPK ? 2 : 1) * PAIR_T;  // uint4 per buffer: [half][PAIR_T]
     uint4 *ring0 = smem;                         // slot 0
     uint4 *ring23 = smem + RB;                   // [row & 1][slot 2, 3]
     uint4 *ring1 = smem + 5 * RB;                // [row % 3]
-    uint4 *stage = smem + 8 * RB;                // [2][NST][PAIR_T]
+    uint4 *stage = smem + 8 * RB;                // [PAIR_NBUF][NST][PAIR_T]
     const int NG = PAIR_T >> LOG2G, NI = NG - 2;
     const int tid = threadIdx.x;
     const int g = tid >> LOG2G, lane_g = tid & (G - 1);
@@ -899,17 +912,24 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
 #pragma unroll 1
     for (int ya = Y0 - 1; ya <= Y1; ++ya, ++s) {
         cp_async_wait_all();  // this step's inputs (this thread's own copies)
-        if (ya + 1 <= Y1) issue(ya + 1, (s + 1) & 1);
-        const uint4 *st = stage + (size_t)(s & 1) * NST * PAIR_T + tid;
+        const uint4 *st = stage + (size_t)(PAIR_NBUF == 2 ? (s & 1) : 0) * NST * PAIR_T + tid;
+        uint4 sv[NST];  // NBUF 1: the step's staged inputs, moved to registers before the refill
+        if (PAIR_NBUF == 1) {
+#pragma unroll
+            for (int k = 0; k < NST; ++k) sv[k] = st[k * PAIR_T];
+            st = sv;
+        }
+        if (ya + 1 <= Y1) issue(ya + 1, PAIR_NBUF == 2 ? (s + 1) & 1 : 0);
+        constexpr int SS = PAIR_NBUF == 2 ? PAIR_T : 1;  // stride between staged chunks
         // ---- A-phase: colour-A pixel index I0-1+g of row ya (incl. the halo pixels)
         if (ya >= 0 && ya < a.H) {
             uint32_t dv[8], in[4][8];
 #pragma unroll
-            for (int k = 0; k < 4; ++k) unpack_u8(MODEA == 1 ? make_uint4(0u, 0u, 0u, 0u) : st[k * PAIR_T], in[k]);
+            for (int k = 0; k < 4; ++k) unpack_u8(MODEA == 1 ? make_uint4(0u, 0u, 0u, 0u) : st[k * SS], in[k]);
             if (sizeof(TD) == 1) {
-                unpack_u8(st[4 * PAIR_T], dv);
+                unpack_u8(st[4 * SS], dv);
             } else {
-                const uint4 lo = st[4 * PAIR_T], hi = st[5 * PAIR_T];
+                const uint4 lo = st[4 * SS], hi = st[5 * SS];
                 dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
@@ -961,9 +981,9 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
                 }
             }
             if (sizeof(TD) == 1) {
-                unpack_u8(st[(4 + DW) * PAIR_T], dv);
+                unpack_u8(st[(4 + DW) * SS], dv);
             } else {
-                const uint4 lo = st[(4 + DW) * PAIR_T], hi = st[(5 + DW) * PAIR_T];
+                const uint4 lo = st[(4 + DW) * SS], hi = st[(5 + DW) * SS];
                 dv[0] = lo.x, dv[1] = lo.y, dv[2] = lo.z, dv[3] = lo.w;
                 dv[4] = hi.x, dv[5] = hi.y, dv[6] = hi.z, dv[7] = hi.w;
             }
@@ -985,7 +1005,7 @@ __global__ void __launch_bounds__(PAIR_T, 2) k_update_pair(FastArgs a, const TD 
 size_t pair_smem_bytes(int dbytes)
 {
     const int DW = dbytes == 1 ? 1 : 2;
-    return (size_t)(8 * (dbytes == 1 ? 2 : 1) + 2 * (4 + 2 * DW)) * PAIR_T * sizeof(uint4);
+    return (size_t)(8 * (dbytes == 1 ? 2 : 1) + PAIR_NBUF * (4 + 2 * DW)) * PAIR_T * sizeof(uint4);
 }
 
 cudaError_t launch_update_pair(const void *D, int dbytes, const FastArgs &a, int B, int mode, bool sgn, int band,
