@@ -9,21 +9,23 @@
 // (pair, row, column) order, with offsets[b] = index of pair b's first point and
 // offsets[B] = the total.
 //
-// Three short kernels, no inter-CTA waiting: the flattened (pair, pixel) range is
-// cut into tiles of CC_TILE consecutive pixels that never straddle a pair boundary;
-//   k_compact_count  counts each tile's valid pixels (skipped when the JBU kernel
-//                    has already accumulated the counts while producing disp --
-//                    jbu_compact_batch: the a6 kernel is EX2-bound, counting is free);
-//   k_compact_scan   one CTA: exclusive prefix of the tile counts -> each tile's
-//                    first output index, offsets[B+1] and n_valid[B];
-//   k_compact_write  re-derives each tile's in-tile ranks (ballots, round-strided
-//                    pixel ownership), evaluates Eq.3 for its valid pixels into
-//                    shared memory and stores the tile's points as one contiguous
-//                    coalesced run.
+// Three short kernels, no inter-CTA waiting: every row of every pair is cut into
+// SEGMENTS of CC_SEG = 128 consecutive pixels (the last one of a row shorter), so the
+// segments in (pair, row, segment) order are the pixels in raster order;
+//   k_compact_count  counts each segment's valid pixels, one warp per segment (skipped
+//                    when the JBU kernel has already counted them while producing
+//                    disp -- jbu_compact_batch: one warp row of the JBU is one segment,
+//                    the a6 kernel is EX2-bound, counting is free);
+//   k_compact_chunk / k_compact_scan  exclusive prefix of the segment counts -> each
+//                    segment's first output index, offsets[B+1] and n_valid[B];
+//   k_compact_write  one warp per segment: 4 coalesced loads per lane, ballots give
+//                    each valid pixel its rank inside the segment, Eq.3 in registers,
+//                    the points stored at their packed index (the warp's stores cover
+//                    one contiguous run).
 // HBM traffic: 4 B read per pixel (8 B with the count pass) + 12 B written per valid
-// point.  (A single-pass decoupled look-back was built first and measured slower:
-// 2.8-4.3 ms per 128-pair launch, CTAs stalled at the barrier behind warp 0's
-// look-back.)
+// point.  (Round 2 built 2048-pixel tiles first -- per-tile block scans, shared-memory
+// staging, two atomics per JBU warp row -- and a single-pass decoupled look-back before
+// that: DESIGN §12.)
 #include <cstdint>
 
 #include "vsbp_internal.cuh"
@@ -31,13 +33,16 @@
 
 namespace vsbp {
 
-constexpr int CC_T = 256;                // threads per CTA
-constexpr int CC_E = 8;                  // pixels per thread (the tile's packed points fit 24 KB of smem)
-constexpr int CC_TILE = CC_T * CC_E;     // pixels per tile
+constexpr int CC_T = 256;                // threads per CTA (8 warps)
+constexpr int CC_SEG = 128;              // pixels per segment: one warp, 4 per lane
+#ifndef VSBP_CC_WS
+#define VSBP_CC_WS 4
+#endif
+constexpr int CC_WS = VSBP_CC_WS;        // segments per warp in the write kernel
 struct CompactArgs {
     float q[16];
     float min_disp;
-    int W, HW, tiles_per_pair, B;
+    int W, HW, segs, tiles_per_pair, B;  // segs = segments per row, tiles_per_pair = H * segs
     long long cap;                       // capacity of xyz in points
 };
 
@@ -48,28 +53,33 @@ __device__ __forceinline__ float cc_rcp(float d)
     return r;
 }
 
-// tile t -> (pair b, first pixel p0 inside the pair, pixel count n)
-__device__ __forceinline__ void tile_of(const CompactArgs &a, int t, int &b, int &p0, int &n)
+// segment t -> (pair b, index tl inside the pair, first pixel p0 inside the pair,
+// pixel count n)
+__device__ __forceinline__ void seg_of(const CompactArgs &a, int t, int &b, int &tl, int &p0, int &n)
 {
     b = t / a.tiles_per_pair;
-    p0 = (t - b * a.tiles_per_pair) * CC_TILE;
-    n = min(CC_TILE, a.HW - p0);
+    tl = t - b * a.tiles_per_pair;
+    const int y = tl / a.segs, x0 = (tl - y * a.segs) * CC_SEG;
+    p0 = y * a.W + x0;
+    n = min(CC_SEG, a.W - x0);
 }
 
-__global__ void __launch_bounds__(CC_T) k_compact_count(const float *__restrict__ disp, const CompactArgs a,
+__global__ void __launch_bounds__(CC_T) k_compact_count(const float *__restrict__ disp, const CompactArgs a, int tiles,
                                                         int *__restrict__ tile_cnt)
 {
-    int b, p0, n;
-    tile_of(a, blockIdx.x, b, p0, n);
+    const int t = blockIdx.x * (CC_T / 32) + (threadIdx.x >> 5), lane = threadIdx.x & 31;
+    if (t >= tiles) return;
+    int b, tl, p0, n;
+    seg_of(a, t, b, tl, p0, n);
     const float *src = disp + (size_t)b * a.HW + p0;
     int c = 0;
 #pragma unroll
-    for (int i = 0; i < CC_E; ++i) {
-        const int e = i * CC_T + threadIdx.x;
+    for (int k = 0; k < CC_SEG / 32; ++k) {
+        const int e = 32 * k + lane;
         c += (e < n && __ldcs(src + e) >= a.min_disp) ? 1 : 0;
     }
     c = __reduce_add_sync(FULL, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(tile_cnt + blockIdx.x, c);
+    if (lane == 0) tile_cnt[t] = c;
 }
 
 // The tile-count scan in two short kernels over chunks of CS_CHUNK tiles (a few
@@ -146,105 +156,63 @@ __global__ void __launch_bounds__(CS_T) k_compact_scan(const int *__restrict__ t
     }
 }
 
-// Round i of a tile covers its pixels [i*CC_T, (i+1)*CC_T): lane l of warp w owns
-// pixel i*CC_T + 32w + l, so every load is one coalesced 128-byte line per warp and
-// the points of a round land at consecutive shared-memory slots (stride 3 floats:
-// no bank conflicts).  Raster order = (round, warp, lane) order.
+// One warp per segment (CC_WS segments per warp): lane l loads pixels l, l+32, l+64,
+// l+96 of its segment (coalesced), so the raster order inside the segment is
+// (k, lane) and a valid pixel's rank is the popcounts of the earlier ballots plus the
+// lanes below it in its own.  The valid points of one k land at consecutive indices:
+// each store instruction covers one contiguous run.
 __global__ void __launch_bounds__(CC_T) k_compact_write(const float *__restrict__ disp, const __grid_constant__ CompactArgs a,
-                                                        const long long *__restrict__ tile_off, float *__restrict__ xyz,
-                                                        const long long *__restrict__ offsets,
+                                                        int tiles, const long long *__restrict__ tile_off,
+                                                        float *__restrict__ xyz, const long long *__restrict__ offsets,
                                                         unsigned long long *__restrict__ n_valid)
 {
-    constexpr int NW = CC_T / 32;
-    __shared__ float sOut[CC_TILE * 3];
-    __shared__ int sPre[CC_E * NW + 1];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int t = blockIdx.x;
-    int b, p0, n;
-    tile_of(a, t, b, p0, n);
-    const float *src = disp + (size_t)b * a.HW + p0;
-    if (p0 == 0 && tid == 0) n_valid[b] = (unsigned long long)(offsets[b + 1] - offsets[b]);
-
-    // ---- load: one pixel per thread and round; ballot the valid ones
-    float d[CC_E];
-    unsigned ball[CC_E];
-#pragma unroll
-    for (int i = 0; i < CC_E; ++i) {
-        const int e = i * CC_T + tid;
-        d[i] = e < n ? __ldcs(src + e) : 0.f;
-        ball[i] = __ballot_sync(FULL, e < n && d[i] >= a.min_disp);
-    }
-    if (lane == 0) {
-#pragma unroll
-        for (int i = 0; i < CC_E; ++i) sPre[i * NW + warp] = __popc(ball[i]);
-    }
-    __syncthreads();
-    // ---- exclusive scan of the CC_E x NW (round, warp) counts, in raster order (warp 0)
-    if (warp == 0) {
-        static_assert(CC_E * NW == 64, "two counts per lane");
-        const int c0 = sPre[2 * lane], c1 = sPre[2 * lane + 1];
-        int incl = c0 + c1;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(FULL, incl, o);
-            if (lane >= o) incl += v;
-        }
-        const int excl = incl - c0 - c1;
-        sPre[2 * lane] = excl;
-        sPre[2 * lane + 1] = excl + c0;
-        if (lane == 31) sPre[CC_E * NW] = incl;
-    }
-    __syncthreads();
-    const int total = sPre[CC_E * NW];
-
-    // ---- Eq.3 for the valid pixels into their packed slots
-    int v = (p0 + tid) / a.W;
-    int u = p0 + tid - v * a.W;
+    const int lane = threadIdx.x & 31;
     const unsigned lt = (1u << lane) - 1u;
+    const int w = blockIdx.x * (CC_T / 32) + (threadIdx.x >> 5);
+#pragma unroll 1
+    for (int i = 0; i < CC_WS; ++i) {
+        const int t = w * CC_WS + i;
+        if (t >= tiles) return;
+        int b, tl, p0, n;
+        seg_of(a, t, b, tl, p0, n);
+        if (tl == 0 && lane == 0) n_valid[b] = (unsigned long long)(offsets[b + 1] - offsets[b]);
+        const float *src = disp + (size_t)b * a.HW + p0;
+        float d[CC_SEG / 32];
+        unsigned ball[CC_SEG / 32];
 #pragma unroll
-    for (int i = 0; i < CC_E; ++i) {
-        if (ball[i] >> lane & 1) {
-            const int k = sPre[i * NW + warp] + __popc(ball[i] & lt);
-            const float fu = (float)u, fv = (float)v;
-            float h[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-                h[r] = fmaf(a.q[4 * r + 2], d[i], fmaf(a.q[4 * r], fu, fmaf(a.q[4 * r + 1], fv, a.q[4 * r + 3])));
-            const float rW = cc_rcp(h[3]);
-            sOut[3 * k] = h[0] * rW;
-            sOut[3 * k + 1] = h[1] * rW;
-            sOut[3 * k + 2] = h[2] * rW;
+        for (int k = 0; k < CC_SEG / 32; ++k) {
+            const int e = 32 * k + lane;
+            d[k] = e < n ? __ldcs(src + e) : 0.f;
+            ball[k] = __ballot_sync(FULL, e < n && d[k] >= a.min_disp);
         }
-        u += CC_T;
-        while (u >= a.W) {
-            u -= a.W;
-            ++v;
+        const long long base = tile_off[t];
+        const int y = p0 / a.W, x0 = p0 - y * a.W;
+        const float fv = (float)y;
+        int r = 0;
+#pragma unroll
+        for (int k = 0; k < CC_SEG / 32; ++k) {
+            if (ball[k] >> lane & 1) {
+                const long long idx = base + r + __popc(ball[k] & lt);
+                const float fu = (float)(x0 + 32 * k + lane);
+                float h[4];
+#pragma unroll
+                for (int q = 0; q < 4; ++q)
+                    h[q] = fmaf(a.q[4 * q + 2], d[k], fmaf(a.q[4 * q], fu, fmaf(a.q[4 * q + 1], fv, a.q[4 * q + 3])));
+                const float rW = cc_rcp(h[3]);
+                if (idx < a.cap) {  // points beyond the capacity are dropped
+                    float *o = xyz + 3 * idx;
+                    __stcs(o, h[0] * rW);
+                    __stcs(o + 1, h[1] * rW);
+                    __stcs(o + 2, h[2] * rW);
+                }
+            }
+            r += __popc(ball[k]);
         }
     }
-    __syncthreads();
-
-    // ---- one contiguous, coalesced store of the tile's 3 * total floats: 8-byte
-    // stores (conflict-free LDS.64 from shared memory) after a one-float head that
-    // aligns the destination
-    const long long base = tile_off[t];
-    const long long lim = min((long long)total, a.cap - base);  // points beyond the capacity are dropped
-    float *dst = xyz + 3 * base;
-    const int nf = lim > 0 ? (int)(3 * lim) : 0;
-    const int head = min(nf, (int)(((uintptr_t)dst >> 2) & 1));
-    if (tid < head) __stcs(dst, sOut[0]);
-    const int n2 = (nf - head) >> 1;
-    float2 *d2 = reinterpret_cast<float2 *>(dst + head);
-    if (head) {
-        for (int q = tid; q < n2; q += CC_T) __stcs(d2 + q, make_float2(sOut[1 + 2 * q], sOut[2 + 2 * q]));
-    } else {
-        const float2 *s2 = reinterpret_cast<const float2 *>(sOut);
-        for (int q = tid; q < n2; q += CC_T) __stcs(d2 + q, s2[q]);
-    }
-    if (tid == 0 && head + 2 * n2 < nf) __stcs(dst + nf - 1, sOut[nf - 1]);
 }
 
-int compact_tiles_per_pair(int W, int H) { return (W * H + CC_TILE - 1) / CC_TILE; }
-int compact_tile_pixels() { return CC_TILE; }
+int compact_segs_per_row(int W) { return (W + CC_SEG - 1) / CC_SEG; }
+int compact_tiles_per_pair(int W, int H) { return H * compact_segs_per_row(W); }
 
 size_t compact_workspace_bytes(int B, int W, int H)
 {
@@ -260,6 +228,7 @@ static CompactArgs make_args(int B, int W, int H, const float Qf[16], float min_
     a.min_disp = min_disp;
     a.W = W;
     a.HW = W * H;
+    a.segs = compact_segs_per_row(W);
     a.tiles_per_pair = compact_tiles_per_pair(W, H);
     a.B = B;
     a.cap = cap;
@@ -291,7 +260,9 @@ cudaError_t launch_compact_from_counts(int B, const float *disp, int W, int H, c
     const unsigned chunks = (unsigned)((tiles + CS_CHUNK - 1) / CS_CHUNK);
     k_compact_chunk<<<chunks, CS_T, 0, st>>>(compact_counts(ws), (int)tiles, csum);
     k_compact_scan<<<chunks, CS_T, 0, st>>>(compact_counts(ws), (int)tiles, csum, a, toff, offsets);
-    k_compact_write<<<(unsigned)tiles, CC_T, 0, st>>>(disp, a, toff, xyz, offsets, n_valid);
+    const long long wpc = (long long)(CC_T / 32) * CC_WS;  // segments per CTA
+    k_compact_write<<<(unsigned)((tiles + wpc - 1) / wpc), CC_T, 0, st>>>(disp, a, (int)tiles, toff, xyz, offsets,
+                                                                          n_valid);
     note_launch(3);
     return cudaGetLastError();
 }
@@ -304,7 +275,8 @@ cudaError_t launch_compact(int B, const float *disp, int W, int H, const float Q
     const long long tiles = (long long)B * a.tiles_per_pair;
     cudaError_t e = compact_zero_counts(B, W, H, ws, st);
     if (e != cudaSuccess) return e;
-    k_compact_count<<<(unsigned)tiles, CC_T, 0, st>>>(disp, a, compact_counts(ws));
+    k_compact_count<<<(unsigned)((tiles + CC_T / 32 - 1) / (CC_T / 32)), CC_T, 0, st>>>(disp, a, (int)tiles,
+                                                                                       compact_counts(ws));
     note_launch();
     return launch_compact_from_counts(B, disp, W, H, Qf, min_disp, xyz, cap, offsets, n_valid, ws, st);
 }

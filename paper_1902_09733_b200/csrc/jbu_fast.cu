@@ -77,27 +77,21 @@ struct JbuFastArgs {
     float min_disp;
     int do_xyz;
     // a8 fused counting (jbu_compact_batch): when tile_cnt != null, every pixel with
-    // D_p >= min_disp is counted into tile_cnt[b * tiles_per_pair + (raster index >> tile_shift)]
+    // D_p >= min_disp is counted into its compaction segment (128 pixels of a row):
+    // tile_cnt[b * pair_segs + y * row_segs + x / 128]
     int *tile_cnt;
-    int tiles_per_pair, tile_shift;
+    int pair_segs, row_segs;
 };
 
-// the valid pixels of one row segment of a warp (lane: c pixels starting at raster
-// column x of row y), counted per compaction tile; a warp's segment (<= 128 px)
-// meets at most two tiles.  Warp-uniform call.
-// Lane 0 is inside whenever any lane is (x grows with the lane), the segment's second
-// tile is the next one (raster order), and a warp counts <= 256 pixels, so both counts
-// travel packed in one reduction (low / high 16 bits).
-__device__ __forceinline__ void count_row(const JbuFastArgs &a, int b, int Wh, int y, int x, int c, bool inside)
+// the valid pixels of one warp row (lane: c pixels of row y; lane 0 at column x0w,
+// x grows with the lane) are counted into the compaction segment of x0w: a warp row
+// (128, 64 or 32 pixels, aligned to its size) never straddles a segment.  Lane 0 is
+// inside whenever any lane is.  Warp-uniform call.
+__device__ __forceinline__ void count_row(const JbuFastArgs &a, int b, int y, int x0w, int c, bool inside0)
 {
-    const int tt = inside ? (int)(((long long)y * Wh + x) >> a.tile_shift) : -1;
-    const int tA = __shfl_sync(FULL, tt, 0);
-    const int sum = __reduce_add_sync(FULL, tt == tA ? c : (c << 16));
-    if ((threadIdx.x & 31) == 0 && tA >= 0) {
-        int *base = a.tile_cnt + (size_t)b * a.tiles_per_pair + tA;
-        if (sum & 0xFFFF) atomicAdd(base, sum & 0xFFFF);
-        if (sum >> 16) atomicAdd(base + 1, sum >> 16);
-    }
+    const int sum = __reduce_add_sync(FULL, c);
+    if ((threadIdx.x & 31) == 0 && inside0 && sum)
+        atomicAdd(a.tile_cnt + (size_t)b * a.pair_segs + (size_t)y * a.row_segs + (x0w >> 7), sum);
 }
 
 __device__ __forceinline__ float ex2(float x)
@@ -337,7 +331,8 @@ __global__ void __launch_bounds__(256) k_jbu_fast(const int32_t *__restrict__ di
         }
         disp_hi[((size_t)b * Hh + y) * Wh + x] = Dp;
     }
-    if (a.tile_cnt) count_row(a, b, Wh, y, x, (inside && Dp >= a.min_disp) ? 1 : 0, inside);
+    if (a.tile_cnt)
+        count_row(a, b, y, x0, (inside && Dp >= a.min_disp) ? 1 : 0, x0 < Wh && y < Hh);  // warp row: 32 px from x0
     if (!a.do_xyz) return;
     float o[3];
     const bool valid = inside && reproject_px(a, (float)x, (float)y, Dp, o);
@@ -453,6 +448,7 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     for (int rp = 0; rp < JB_RP; ++rp) {
     const int yb = y0 + rp * JB_Y + NR * threadIdx.y;
     const bool inside = x < Wh && yb < Hh;  // Wh % P == 0, Hh % NR == 0: all pixels or none
+    const bool inside0 = x0 < Wh && yb < Hh;  // the warp row's first pixel (lane 0)
     float Dp[NR][P];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
@@ -611,7 +607,7 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
             int c = 0;
 #pragma unroll
             for (int k = 0; k < P; ++k) c += (inside && Dp[r][k] >= a.min_disp) ? 1 : 0;
-            count_row(a, b, Wh, yb + r, x, c, inside);
+            count_row(a, b, yb + r, x0, c, inside0);
         }
     }
     if (!a.do_xyz) continue;
@@ -717,8 +713,8 @@ cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const u
     a.min_disp = min_disp;
     a.do_xyz = xyz != nullptr;
     a.tile_cnt = tile_cnt;
-    a.tiles_per_pair = compact_tiles_per_pair(W * s, H * s);
-    a.tile_shift = __builtin_ctz((unsigned)compact_tile_pixels());
+    a.pair_segs = compact_tiles_per_pair(W * s, H * s);
+    a.row_segs = compact_segs_per_row(W * s);
     dim3 block(JB_X, JB_Y);
     // the vector kernel needs P-aligned guide words and 4P-byte aligned outputs
     const auto al = [](const void *p, uintptr_t m) { return ((uintptr_t)p & (m - 1)) == 0; };

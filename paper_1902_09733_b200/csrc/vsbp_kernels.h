@@ -70,7 +70,7 @@ cudaError_t launch_export_msgs(const void *M, int mbytes, const Geom &g, int b, 
 cudaError_t launch_export_costs(const void *D, int dbytes, const Geom &g, int b, int32_t *out, cudaStream_t st);
 
 // tile_cnt (optional): also count the pixels with D >= min_disp per a8 compaction
-// tile (compact.cu), for launch_compact_from_counts
+// segment (128 pixels of a row, compact.cu; zeroed first), for launch_compact_from_counts
 cudaError_t launch_jbu_fast(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide, int s, float *disp_hi,
                             float sigma_s, float sigma_r, int radius, const float *Qf, float min_disp, float *xyz,
                             unsigned long long *n_valid, cudaStream_t st, int *tile_cnt = nullptr);
@@ -79,8 +79,8 @@ cudaError_t launch_reproject(int B, const float *disp, int W, int H, const float
 cudaError_t launch_prep(int n, const uint8_t *rgb, int W_hi, int H_hi, int s, uint8_t *gray, cudaStream_t st);
 // a8 compaction (compact.cu)
 size_t compact_workspace_bytes(int B, int W, int H);
-int compact_tiles_per_pair(int W, int H);
-int compact_tile_pixels();
+int compact_tiles_per_pair(int W, int H);  // segments (128-pixel row pieces) per pair
+int compact_segs_per_row(int W);
 int *compact_counts(void *ws);
 cudaError_t compact_zero_counts(int B, int W, int H, void *ws, cudaStream_t st);
 cudaError_t launch_compact_from_counts(int B, const float *disp, int W, int H, const float Qf[16], float min_disp,
