@@ -859,6 +859,20 @@ __global__ void __launch_bounds__(PAIR_T, PAIR_MINB) k_update_pair(FastArgs a, c
     const uint8_t *MoB = Mr + (size_t)(cB * 4u) * P;        // colour-B planes of iteration t-1
     const TD *DA = Db + cA * P, *DB = Db + cB * P;
 
+    // MODE 2: the parent columns iA - 1, iA, iA + 1 of the thread (chunk offsets,
+    // parities, and whether the parent sends right (px < Wp - 1) / left (px > 0))
+    const uint8_t *Mpb = MODEA == 2 ? a.Mp + (size_t)b * a.pairMp : nullptr;
+    uint32_t pcol0 = 0, pcol1 = 0, pcol2 = 0, ppar0 = 0, ppar1 = 0, ppar2 = 0;
+    bool pr0 = false, pr1 = false, pl1 = false, pl2 = false;
+    if (MODEA == 2) {
+        const int p0 = iA - 1, p1 = iA, p2 = iA + 1;
+        pcol0 = (uint32_t)(p0 >> 1) * Lp + (uint32_t)d0;  // only used when p0 >= 0
+        pcol1 = (uint32_t)(p1 >> 1) * Lp + (uint32_t)d0;
+        pcol2 = (uint32_t)(p2 >> 1) * Lp + (uint32_t)d0;
+        ppar0 = (uint32_t)p0 & 1u, ppar1 = (uint32_t)p1 & 1u, ppar2 = (uint32_t)p2 & 1u;
+        pr0 = p0 < a.Wp - 1, pr1 = p1 < a.Wp - 1, pl1 = p1 > 0, pl2 = p2 > 0;
+    }
+
     // enqueue the global inputs of step `ya` (A row ya, B row ya-1) into stage[buf]
     auto issue = [&](int ya, int buf) {
         uint4 *st = stage + (size_t)buf * NST * PAIR_T + tid;
@@ -873,23 +887,26 @@ __global__ void __launch_bounds__(PAIR_T, PAIR_MINB) k_update_pair(FastArgs a, c
             cp_async16(st + 2 * PAIR_T, MoB + (v2 ? 3u * P + rA + (o - 1u) * Lp : 0u), v2);
             cp_async16(st + 3 * PAIR_T, MoB + (v3 ? 2u * P + rA + o * Lp : 0u), v3);
         } else if (MODEA == 2) {
-            const bool has[4] = {ya > 0, ya < a.H - 1, xA > 0, xA < a.W - 1};
-            const uint8_t *Mpb = a.Mp + (size_t)b * a.pairMp;
-            const int X = xA >> 1, Y = ya >> 1;
-            const int pyu = (ya - 1) >> 1, pyd = (ya + 1) >> 1, pxl = (xA - 1) >> 1, pxr = (xA + 1) >> 1;
-            const uint32_t Wcp = (uint32_t)a.Wcp;
-#pragma unroll
-            for (int k = 0; k < 4; ++k) {
-                const int px = k == 2 ? pxl : (k == 3 ? pxr : X);
-                const int py = k == 0 ? pyu : (k == 1 ? pyd : Y);
-                const int slot = k ^ 1;
-                const bool ph = slot == 0 ? py > 0 : slot == 1 ? py < a.Hp - 1 : slot == 2 ? px > 0 : px < a.Wp - 1;
-                const bool v = okA && has[k] && ph;
-                const uint32_t off = v ? ((uint32_t)(((px + py) & 1) * 4 + slot)) * a.planep +
-                                             ((uint32_t)py * Wcp + (uint32_t)(px >> 1)) * Lp + (uint32_t)d0
-                                       : 0u;
-                cp_async16(st + k * PAIR_T, Mpb + off, v);
-            }
+            // the parent of (xA, y) is (xA >> 1, y >> 1) = (iA, y >> 1): the vertical
+            // neighbours' parents sit in column iA, the left / right ones' in columns
+            // iA - 1 + o / iA + o (per-thread constants pcol / ppar / pr / pl, above);
+            // neighbour k's parent sends on slot k ^ 1
+            const int Y = ya >> 1, pyu = (ya - 1) >> 1, pyd = (ya + 1) >> 1;
+            const uint32_t rowp = (uint32_t)a.Wcp * Lp, PP = a.planep;
+            const uint32_t cm = o ? pcol1 : pcol0, cq = o ? pcol2 : pcol1;  // left / right parents' columns
+            const uint32_t pm = o ? ppar1 : ppar0, pq = o ? ppar2 : ppar1;  // and parities
+            const bool v0 = okA && ya > 0 && pyu < a.Hp - 1;                  // up: the parent's slot 1
+            const bool v1 = okA && ya < a.H - 1 && pyd > 0;                   // down: slot 0
+            const bool v2 = okA && xA > 0 && (o ? pr1 : pr0);                 // left: slot 3 (px < Wp - 1)
+            const bool v3 = okA && xA < a.W - 1 && (o ? pl2 : pl1);           // right: slot 2 (px > 0)
+            const uint32_t o0 = v0 ? (((ppar1 + (uint32_t)pyu) & 1u) * 4u + 1u) * PP + (uint32_t)pyu * rowp + pcol1 : 0u;
+            const uint32_t o1 = v1 ? (((ppar1 + (uint32_t)pyd) & 1u) * 4u) * PP + (uint32_t)pyd * rowp + pcol1 : 0u;
+            const uint32_t o2 = v2 ? (((pm + (uint32_t)Y) & 1u) * 4u + 3u) * PP + (uint32_t)Y * rowp + cm : 0u;
+            const uint32_t o3 = v3 ? (((pq + (uint32_t)Y) & 1u) * 4u + 2u) * PP + (uint32_t)Y * rowp + cq : 0u;
+            cp_async16(st + 0 * PAIR_T, Mpb + o0, v0);
+            cp_async16(st + 1 * PAIR_T, Mpb + o1, v1);
+            cp_async16(st + 2 * PAIR_T, Mpb + o2, v2);
+            cp_async16(st + 3 * PAIR_T, Mpb + o3, v3);
         }
         {
             const uint4 *dp = reinterpret_cast<const uint4 *>(DA + (okA ? rA : 0u));
