@@ -835,8 +835,9 @@ def _check_compaction(disp_np, Q, min_disp=1.0, batch=None):
 @pytest.mark.parametrize("B,W,H,frac", [(1, 7, 5, 0.5), (3, 45, 91, 0.7), (2, 2048, 1, 0.9), (5, 3, 700, 0.2),
                                         (4, 173, 61, 0.0), (2, 64, 64, 1.0), (9, 301, 17, 0.5)])
 def test_compact_cloud_matches_oracle(B, W, H, frac):
-    """Ragged tiles (W*H not a multiple of the 2048-pixel tile), W < the 8 pixels a
-    thread owns, empty and full pairs, tile boundaries inside rows."""
+    """Ragged segments (W not a multiple of the 128-pixel segment: a short last
+    segment per row), W < 32 (lanes without pixels), exactly 16 full segments
+    (W = 2048), one-row and one-column-ish shapes, empty and full pairs."""
     rng = np.random.default_rng(B * W + H)
     d = rng.uniform(1.0, 200.0, size=(B, H, W))
     d[rng.random((B, H, W)) >= frac] = rng.uniform(-5.0, 0.999)
@@ -902,8 +903,9 @@ def test_compact_cloud_full_frames_sampled():
                                        (4, 5, 676, 380, 1)])
 def test_jbu_compact_equals_separate_calls(s, r, W, H, B):
     """jbu_compact_batch (counts folded into the JBU kernel, vector and scalar
-    kernels) == jbu_upsample_batch + compact_cloud_batch, bit for bit, including
-    pairs with invalid regions and tiles that straddle rows."""
+    kernels: a 128-, 64- or 32-pixel warp row per compaction segment) ==
+    jbu_upsample_batch + compact_cloud_batch, bit for bit, including pairs with
+    invalid regions and rows ending in a short segment."""
     rng = np.random.default_rng(s * W + r)
     lo = rng.integers(0, 40, size=(B, H, W)).astype(np.int32)
     lo[0, : H // 3] = 0  # a band of invalid (d < min_disp) pixels
