@@ -368,31 +368,57 @@ __device__ __forceinline__ f2_t add2(f2_t a, f2_t b)
     return d;
 }
 
+// a thread's P guide pixels of one row: raw() issues the loads (3 words), split()
+// turns them into P packed RGB values -- separate, so the vector kernel can fetch the
+// next row pass's guide while it computes this one (the loads' latency hidden)
 template <int P> struct GuideVec;
 template <> struct GuideVec<4> {  // 12 bytes, 4-byte aligned (x % 4 == 0)
+    static __device__ __forceinline__ void raw(const uint8_t *g, unsigned w[3])
+    {
+        const unsigned *p = reinterpret_cast<const unsigned *>(g);
+        w[0] = __ldg(p), w[1] = __ldg(p + 1), w[2] = __ldg(p + 2);
+    }
+    static __device__ __forceinline__ void split(const unsigned w[3], unsigned I[4])
+    {
+        I[0] = w[0] & 0xFFFFFFu;
+        I[1] = __funnelshift_r(w[0], w[1], 24) & 0xFFFFFFu;
+        I[2] = __funnelshift_r(w[1], w[2], 16) & 0xFFFFFFu;
+        I[3] = w[2] >> 8;
+    }
     static __device__ __forceinline__ void load(const uint8_t *g, unsigned I[4])
     {
-        const unsigned *w = reinterpret_cast<const unsigned *>(g);
-        const unsigned w0 = __ldg(w), w1 = __ldg(w + 1), w2 = __ldg(w + 2);
-        I[0] = w0 & 0xFFFFFFu;
-        I[1] = __funnelshift_r(w0, w1, 24) & 0xFFFFFFu;
-        I[2] = __funnelshift_r(w1, w2, 16) & 0xFFFFFFu;
-        I[3] = w2 >> 8;
+        unsigned w[3];
+        raw(g, w);
+        split(w, I);
     }
 };
 template <> struct GuideVec<2> {  // 6 bytes, 2-byte aligned
-    static __device__ __forceinline__ void load(const uint8_t *g, unsigned I[2])
+    static __device__ __forceinline__ void raw(const uint8_t *g, unsigned w[3])
     {
         const unsigned short *h = reinterpret_cast<const unsigned short *>(g);
-        const unsigned h0 = __ldg(h), h1 = __ldg(h + 1), h2 = __ldg(h + 2);
-        I[0] = h0 | ((h1 & 0xFFu) << 16);
-        I[1] = (h1 >> 8) | (h2 << 8);
+        w[0] = __ldg(h), w[1] = __ldg(h + 1), w[2] = __ldg(h + 2);
+    }
+    static __device__ __forceinline__ void split(const unsigned w[3], unsigned I[2])
+    {
+        I[0] = w[0] | ((w[1] & 0xFFu) << 16);
+        I[1] = (w[1] >> 8) | (w[2] << 8);
+    }
+    static __device__ __forceinline__ void load(const uint8_t *g, unsigned I[2])
+    {
+        unsigned w[3];
+        raw(g, w);
+        split(w, I);
     }
 };
+#ifndef VSBP_JBU_GPREF
+#define VSBP_JBU_GPREF 1  // vector kernel: guide of row pass rp + 1 loaded during pass rp
+#endif
 
 template <int R, int S, int NR, int P>
 #ifndef VSBP_JBU_MINB
-#define VSBP_JBU_MINB 5  // resident CTAs per SM for the 2-row, 4-pixel variant (the bench's s = 4)
+// resident CTAs per SM for the 2-row, 4-pixel variant (the bench's s = 4): 4 leaves
+// 128 registers, room for the next row pass's guide words (5: 96, spills)
+#define VSBP_JBU_MINB 4
 #endif
 __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU_MINB : 8) : (P == 4 ? 3 : 4)) k_jbu_vec(const int32_t *__restrict__ disp_lo,
                                                            const uint8_t *__restrict__ guide,
@@ -444,11 +470,28 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         for (int r = 0; r < NR; ++r) ryv[r][t] = a.ryt[v0 + r][t];
 #endif
     }
+    unsigned gw[NR][3];  // VSBP_JBU_GPREF: the raw guide words of the next row pass
+    if (VSBP_JBU_GPREF) {
+        const int yb = y0 + NR * threadIdx.y;
+#pragma unroll
+        for (int r = 0; r < NR; ++r)
+            if (x < Wh && yb < Hh) GuideVec<P>::raw(G + ((size_t)(yb + r) * Wh + x) * 3, gw[r]);
+    }
 #pragma unroll 1
     for (int rp = 0; rp < JB_RP; ++rp) {
     const int yb = y0 + rp * JB_Y + NR * threadIdx.y;
     const bool inside = x < Wh && yb < Hh;  // Wh % P == 0, Hh % NR == 0: all pixels or none
     const bool inside0 = x0 < Wh && yb < Hh;  // the warp row's first pixel (lane 0)
+    unsigned Ipf[NR][P];
+    if (VSBP_JBU_GPREF) {
+#pragma unroll
+        for (int r = 0; r < NR; ++r) GuideVec<P>::split(gw[r], Ipf[r]);
+        const int yn = yb + JB_Y;
+        if (rp + 1 < JB_RP && x < Wh && yn < Hh) {
+#pragma unroll
+            for (int r = 0; r < NR; ++r) GuideVec<P>::raw(G + ((size_t)(yn + r) * Wh + x) * 3, gw[r]);
+        }
+    }
     float Dp[NR][P];
 #pragma unroll
     for (int r = 0; r < NR; ++r)
@@ -457,7 +500,14 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
     if (inside) {
         unsigned Ip[NR][P];
 #pragma unroll
-        for (int r = 0; r < NR; ++r) GuideVec<P>::load(G + ((size_t)(yb + r) * Wh + x) * 3, Ip[r]);
+        for (int r = 0; r < NR; ++r) {
+            if (VSBP_JBU_GPREF) {
+#pragma unroll
+                for (int k = 0; k < P; ++k) Ip[r][k] = Ipf[r][k];
+            } else {
+                GuideVec<P>::load(G + ((size_t)(yb + r) * Wh + x) * 3, Ip[r]);
+            }
+        }
         const int cy = yb / S;
 #if VSBP_JBU_UNROLL_TY
         float rfl[NR][T];
