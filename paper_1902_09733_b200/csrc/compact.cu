@@ -132,8 +132,13 @@ __global__ void __launch_bounds__(CS_T) k_compact_scan(const int *__restrict__ t
                                                        long long *__restrict__ tile_off, long long *__restrict__ offsets)
 {
     __shared__ long long sW[33];
-    long long base = 0;
-    for (int c = 0; c < (int)blockIdx.x; ++c) base += chunk_sum[c];  // a few dozen chunks
+    // this chunk's base: the sum of the earlier chunks' totals, summed by the whole
+    // block (hundreds of chunks at the bench's 4.3 M segments)
+    long long part = 0;
+    for (int c = threadIdx.x; c < (int)blockIdx.x; c += CS_T) part += chunk_sum[c];
+    long long base;
+    block_excl_scan(part, sW, base);
+    __syncthreads();  // sW is reused below
     const int t0 = blockIdx.x * CS_CHUNK + threadIdx.x * CS_V;
     int v[CS_V];
     long long c = 0;

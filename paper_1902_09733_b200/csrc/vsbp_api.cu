@@ -76,7 +76,7 @@ int bytes_for_max(long long vmax)
 
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
-bool use_pair(const vsbp_bp *c, int l);
+bool use_pair(const vsbp_bp *c, int l, int B);
 
 void plan(vsbp_bp *c, int batch)
 {
@@ -91,7 +91,7 @@ void plan(vsbp_bp *c, int batch)
     }
     for (int l = 0; l < c->levels; ++l) {
         c->m2_off[l] = 0;
-        if (use_pair(c, l)) {
+        if (use_pair(c, l, batch)) {  // monotone in B: a call with B <= batch never needs more
             c->m2_off[l] = off;
             off = align256(off + (size_t)batch * 8 * c->Hl[l] * c->Wcl[l] * c->Lp * c->msg_bytes);
         }
@@ -155,18 +155,21 @@ bool use_final(const vsbp_bp *c)
 // at least three iterations (the last one of every level stays a single launch: its
 // messages must all be stored -- the WTA, the up-copy and the exports read both
 // colours), and one Lp chunk per lane group that fits the CTA
-bool use_pair(const vsbp_bp *c, int l)
+bool use_pair(const vsbp_bp *c, int l, int B)
 {
     if (!c->pair_fuse || !use_fast(c, l) || c->iters < 3 || c->G > 32) return false;
     if (l == 0 && use_dimg(c) && !dimg_only_singles(c)) return false;
-    // 1 (default): levels of >= pair_min_px pixels only -- a CTA walks its band row by row,
-    // so small levels have too few CTAs to fill the GPU (levels 2-4 of C2 measured
-    // 1.8-2.3x slower fused); 2: every level (tests)
-    // u16-cost levels measured slower fused (C2 level 1 1.91 -> 2.05 ms, C4 level 1
-    // 0.193 -> 0.208 ms per pair): their staging doubles and the ring stays packed
-    // 3: as 1, u16-cost levels included
-    return c->pair_fuse == 2 ||
-           ((c->dbytes[l] == 1 || c->pair_fuse == 3) && (long long)c->Wl[l] * c->Hl[l] >= c->pair_min_px);
+    if (c->pair_fuse == 2) return true;  // every level (tests)
+    // a CTA walks its band row by row, so small levels have too few CTAs to fill the
+    // GPU (levels 2-4 of C2 measured 1.8-2.3x slower fused)
+    const long long px = (long long)c->Wl[l] * c->Hl[l];
+    if (c->dbytes[l] == 1) return px >= c->pair_min_px;
+    if (c->pair_fuse == 3) return false;  // u8-cost levels only
+    // 1 (default): u16-cost levels too, when the call holds >= 2M of their pixels and
+    // each pair >= 50K (C5 level 1 fused 8466 -> 8586 pairs/s, C4 level 1
+    // 0.191 -> 0.183 ms per pair; C4 level 2 (64K px x 8 pairs) 0.052 -> 0.066 ms and
+    // C5 level 2 (16K px) slower)
+    return px >= 50000 && px * B >= 2000000;
 }
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
@@ -491,7 +494,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
         const bool fast = use_fast(c, l);
         for (int t = 0; t < c->iters; ++t) {
             const int mode = (t > 0) ? 0 : (l == top ? 1 : 2);
-            if (fast && use_pair(c, l) && t + 1 < c->iters - 1) {
+            if (fast && use_pair(c, l, B) && t + 1 < c->iters - 1) {
                 // iterations t and t+1 in one launch; the level's messages move to its
                 // other array (colour t&1's are consumed on chip and never stored)
                 vsbp::FastArgs fa = fast_args(c, l, ws, disp);
