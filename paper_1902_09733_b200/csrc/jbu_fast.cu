@@ -471,17 +471,25 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
 #endif
     }
     unsigned gw[NR][3];  // VSBP_JBU_GPREF: the raw guide words of the next row pass
+    // row-pass cursors (advanced by JB_Y rows per pass, no per-pass 64-bit index math):
+    // the next pass's guide pixels and this pass's output row
+    const size_t grow = (size_t)Wh * 3;
+    const uint8_t *gnext = G + ((size_t)(y0 + NR * threadIdx.y) * Wh + x) * 3;
+    float *dcur = disp_hi + ((size_t)b * Hh + y0 + NR * threadIdx.y) * Wh + x;
     if (VSBP_JBU_GPREF) {
         const int yb = y0 + NR * threadIdx.y;
 #pragma unroll
         for (int r = 0; r < NR; ++r)
-            if (x < Wh && yb < Hh) GuideVec<P>::raw(G + ((size_t)(yb + r) * Wh + x) * 3, gw[r]);
+            if (x < Wh && yb < Hh) GuideVec<P>::raw(gnext + r * grow, gw[r]);
+        gnext += (size_t)JB_Y * grow;
     }
 #pragma unroll 1
     for (int rp = 0; rp < JB_RP; ++rp) {
     const int yb = y0 + rp * JB_Y + NR * threadIdx.y;
     const bool inside = x < Wh && yb < Hh;  // Wh % P == 0, Hh % NR == 0: all pixels or none
     const bool inside0 = x0 < Wh && yb < Hh;  // the warp row's first pixel (lane 0)
+    float *const drow = dcur;  // this pass's first output row
+    dcur += (size_t)JB_Y * Wh;
     unsigned Ipf[NR][P];
     if (VSBP_JBU_GPREF) {
 #pragma unroll
@@ -489,8 +497,9 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         const int yn = yb + JB_Y;
         if (rp + 1 < JB_RP && x < Wh && yn < Hh) {
 #pragma unroll
-            for (int r = 0; r < NR; ++r) GuideVec<P>::raw(G + ((size_t)(yn + r) * Wh + x) * 3, gw[r]);
+            for (int r = 0; r < NR; ++r) GuideVec<P>::raw(gnext + r * grow, gw[r]);
         }
+        gnext += (size_t)JB_Y * grow;
     }
     float Dp[NR][P];
 #pragma unroll
@@ -644,7 +653,7 @@ __global__ void __launch_bounds__(JB_X * JB_Y / NR, NR == 2 ? (P == 4 ? VSBP_JBU
         }
 #pragma unroll
         for (int r = 0; r < NR; ++r) {
-            float *dst = disp_hi + ((size_t)b * Hh + yb + r) * Wh + x;
+            float *dst = drow + (size_t)r * Wh;
             if (P == 4)
                 *reinterpret_cast<float4 *>(dst) = make_float4(Dp[r][0], Dp[r][1], Dp[r][2], Dp[r][3]);
             else
