@@ -107,14 +107,15 @@ int bp_create(int W, int H, int ndisp, int levels, int iters, float lambda, floa
  *                        messages stay on chip, so a pair moves 10L instead of 18L
  *                        bytes per pixel pair at u8 (levels with u8 costs and >=
  *                        VSBP_OPT_PAIR_MINPX pixels; levels with u16 costs and
- *                        >= 50000 pixels when the call's batch holds >= 2M of
+ *                        >= 10000 pixels when the call's batch holds >= 2M of
  *                        their pixels).  The level's messages then alternate
  *                        between two arrays (bp_workspace_bytes grows by one
  *                        message array per such level at the workspace's batch).
  *                        2 = on every eligible level (tests); 3 = u8-cost levels
  *                        only; 0 = one iteration per launch.  Results are
  *                        identical.
- *   VSBP_OPT_PAIR_BAND : rows per CTA of the two-iteration kernel (default 64).
+ *   VSBP_OPT_PAIR_BAND : rows per CTA of the two-iteration kernel (default 64;
+ *                        levels shorter than two bands use 16).
  *   VSBP_OPT_PAIR_MINPX: smallest level (W_l * H_l pixels) fused under
  *                        VSBP_OPT_PAIR = 1 (default 100000). */
 #define VSBP_OPT_PAIR 5

@@ -77,6 +77,7 @@ int bytes_for_max(long long vmax)
 size_t align256(size_t v) { return (v + 255) & ~(size_t)255; }
 
 bool use_pair(const vsbp_bp *c, int l, int B);
+int pair_band_of(const vsbp_bp *c, int l);
 
 void plan(vsbp_bp *c, int batch)
 {
@@ -166,11 +167,15 @@ bool use_pair(const vsbp_bp *c, int l, int B)
     if (c->dbytes[l] == 1) return px >= c->pair_min_px;
     if (c->pair_fuse == 3) return false;  // u8-cost levels only
     // 1 (default): u16-cost levels too, when the call holds >= 2M of their pixels and
-    // each pair >= 50K (C5 level 1 fused 8466 -> 8586 pairs/s, C4 level 1
-    // 0.191 -> 0.183 ms per pair; C4 level 2 (64K px x 8 pairs) 0.052 -> 0.066 ms and
-    // C5 level 2 (16K px) slower)
-    return px >= 50000 && px * B >= 2000000;
+    // each pair >= 10K (C5 level 1 fused 8466 -> 8586 pairs/s, level 2 with
+    // 16-row bands 8611 -> 8638; C4 level 1 0.191 -> 0.183 ms per pair; C4 level 2
+    // (64K px x 8 pairs) 0.052 -> 0.066 ms)
+    return px >= 10000 && px * B >= 2000000;
 }
+
+// rows per CTA band of k_update_pair on level l: pair_band, and 16 on levels shorter
+// than two bands (4x the CTAs for the serial row walk: C5 level 2 fused gained only so)
+int pair_band_of(const vsbp_bp *c, int l) { return c->Hl[l] < 2 * c->pair_band ? 16 : c->pair_band; }
 
 // beliefs of level l fit 15 bits: the signed one-instruction normalise applies
 bool fast_signed(const vsbp_bp *c, int l)
@@ -499,7 +504,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 // other array (colour t&1's are consumed on chip and never stored)
                 vsbp::FastArgs fa = fast_args(c, l, ws, disp);
                 fa.colour = (uint32_t)(t & 1);
-                CK(vsbp::launch_update_pair(D, c->dbytes[l], fa, B, mode, fast_signed(c, l), c->pair_band, st));
+                CK(vsbp::launch_update_pair(D, c->dbytes[l], fa, B, mode, fast_signed(c, l), pair_band_of(c, l), st));
                 c->mcur[l] ^= 1;
                 long long nA = 0, nB = 0;
                 for (int y = 0; y < g.H; ++y) {
@@ -527,7 +532,7 @@ int bp_disparity_batch(vsbp_bp *c, int B, const uint8_t *left, const uint8_t *ri
                 if (wta && use_final(c)) {
                     // last iteration + WTA of both colours, messages not stored
                     if (c->final_fuse == 3)  // row wavefront: A labelled with its update, B from the ring
-                        CK(vsbp::launch_update_pair(D, 1, fa, B, 0, fast_signed(c, l), c->pair_band, st, true));
+                        CK(vsbp::launch_update_pair(D, 1, fa, B, 0, fast_signed(c, l), pair_band_of(c, l), st, true));
                     else if (c->final_fuse == 2)
                         CK(vsbp::launch_final_tile(D, fa, B, fast_signed(c, l), st));
                     else

@@ -85,15 +85,16 @@ def test_level_dims_and_workspace():
     assert n1 > 0 and n4 >= 4 * n1 - 4096 * 10
     msgs = sum(8 * h_ * ((w_ + 1) // 2) * 64 for w_, h_ in dims if w_ * h_ >= 100000)  # one u8 array per large level
     assert msgs - 256 * 5 <= n1p - n1 <= msgs + 256 * 5
-    # u16-cost levels (level 1 here: 338 x 190 = 64K px) get the second array only
-    # when the batch holds >= 2M of their pixels (32 pairs), u8 levels from 100K px
-    m1 = 8 * dims[1][1] * ((dims[1][0] + 1) // 2) * 64
-    for B, fused1 in ((31, False), (32, True)):
+    # u16-cost levels (level 1 here: 338 x 190 = 64K px, level 2: 169 x 95 = 16K px)
+    # get the second array only when the batch holds >= 2M of their pixels (32 / 125
+    # pairs) and they have >= 10K px (level 3: 4K, never); u8 levels from 100K px
+    mm = [8 * hh * ((w + 1) // 2) * 64 for w, hh in dims]
+    for B, fused in ((31, ()), (32, (1,)), (124, (1,)), (125, (1, 2))):
         base = L.bp_workspace_bytes(h, B)
         assert L.bp_set_option(h, P.VSBP_OPT_PAIR, 1) == 0
         extra = L.bp_workspace_bytes(h, B) - base
         assert L.bp_set_option(h, P.VSBP_OPT_PAIR, 0) == 0
-        want = B * (msgs + (m1 if fused1 else 0))
+        want = B * (msgs + sum(mm[l] for l in fused))
         assert want - 256 * 5 <= extra <= want + 256 * 5, (B, extra, want)
     # message option: narrower than lossless is refused, wider accepted
     assert L.bp_set_option(h, P.VSBP_OPT_MSG_BYTES, 2) == 0
