@@ -17,9 +17,9 @@ timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/b
 ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 256"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
-# k_update_pair launches per step: level 1 (u16: MODE 2, MODE 0), then level 0 (MODE 2,
+# k_update_pair launches per step: levels 2 and 1 (u16: MODE 2, MODE 0 each), then level 0 (MODE 2,
 # MODE 0, FIN = the last iteration + both WTAs)
-for cap in ${CAPS:-k_update_pair:3 k_update_pair:4 k_jbu_vec:1 k_compact_write:1}; do
+for cap in ${CAPS:-k_update_pair:5 k_update_pair:6 k_jbu_vec:1 k_compact_write:1}; do
     K=${cap%%:*}; S=${cap##*:}
     timeout 900 ncu --set full --clock-control none --import-source on -k regex:$K -s $S -c 1 \
         -o gpurun_out/prof_${TAG}_${K}_s$S python bench.py $ARGS > gpurun_out/ncu_full_${TAG}_${K}_s$S.log 2>&1
