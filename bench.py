@@ -49,6 +49,23 @@ CAMERA = (1400.0, 1400.0, 1351.5, 759.5, -0.25, 0.08, -0.01)  # f1: GoPro-like r
 WORKLOAD = ("C5: stream of 4096 virtual-stereo pairs of a synthetic 2.7K video (pair k = frames k, k+1), full "
             "pipeline a0-a8 (prep s=4 -> BP 676x380 L=64 5 levels x 5 iters -> JBU r=2 to 2704x1520 -> Eq.3 + "
             "packed point cloud -> summary -> gather)")
+LABELS = (8, 48)  # the video's true disparity range at the BP resolution (C2/C3: [8, 48] of L = 64)
+JBU_RADIUS = None  # --jbu-radius (None: ceil(5 / s))
+CONFIG = 5
+
+
+def set_config(n: int):
+    """--config: 5 (default) = BASELINE configs[4], the C5 stream above; 4 = configs[3],
+    the same video stream through the same pipeline at 1352x760 (s = 2), L = 128,
+    6 levels x 8 iterations, JBU r = 3 to 2.7K (BASELINE.json configs)."""
+    global S_DOWN, NDISP, LEVELS, ITERS, WORKLOAD, LABELS, CONFIG
+    CONFIG = n
+    if n == 4:
+        S_DOWN, NDISP, LEVELS, ITERS = 2, 128, 6, 8
+        LABELS = (16, 96)
+        WORKLOAD = ("C4: stream of virtual-stereo pairs of a synthetic 2.7K video (pair k = frames k, k+1), full "
+                    "pipeline a0-a8 (prep s=2 -> BP 1352x760 L=128 6 levels x 8 iters -> JBU r=3 to 2704x1520 -> "
+                    "Eq.3 + packed point cloud -> summary -> gather)")
 
 
 def parse():
@@ -56,8 +73,16 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=60)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--batch", type=int, default=128,
-                   help="pairs per GPU per step (measured: 32 / 64 / 96 / 128 / 160 -> 6865 / 7041 / 7102 / 7135 / 7127 pairs/s)")
+    p.add_argument("--config", type=int, choices=[4, 5], default=5,
+                   help="BASELINE.json config: 5 = the C5 stream (default, the headline); 4 = the C4 resolution "
+                        "(1352x760, L = 128, 6 x 8) on the same stream")
+    p.add_argument("--batch", type=int, default=0,
+                   help="pairs per GPU per step (default 128 at C5 -- measured 32 / 64 / 96 / 128 / 160 -> "
+                        "6865 / 7041 / 7102 / 7135 / 7127 pairs/s in round 1 -- and 16 at C4, whose BP state is "
+                        "1.4 GB per pair)")
+    p.add_argument("--jbu-radius", type=int, default=0, help="JBU window radius (default ceil(5 / s): 2 at C5)")
+    p.add_argument("--msg-bytes", type=int, default=0, choices=[0, 1, 2, 4],
+                   help="BP message storage bytes (0: the smallest lossless, u8 here)")
     p.add_argument("--pairs", type=int, default=4096, help="length of the synthetic stream (C5: 4096 pairs)")
     p.add_argument("--seed", type=int, default=1902)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
@@ -141,7 +166,7 @@ class ClockSampler:
 
 def video_scene(seed: int):
     from synthgen.video import VideoScene
-    return VideoScene(seed, W_HI, H_HI, S_DOWN, 8, 48)  # C2/C3 label range [8, 48] of L = 64
+    return VideoScene(seed, W_HI, H_HI, S_DOWN, *LABELS)
 
 
 def host_frames(seed: int, k0: int, n: int):
@@ -208,7 +233,8 @@ def oracle_rate(n_threads: int, pairs_per_thread: int, frames):
     def work(k):
         for j in range(pairs_per_thread):
             i = (k + j) % (len(frames) - 1)
-            d, hi, xyz, n = oracle.pipeline_pair(frames[i], frames[i + 1], S_DOWN, NDISP, LEVELS, ITERS, Q)
+            d, hi, xyz, n = oracle.pipeline_pair(frames[i], frames[i + 1], S_DOWN, NDISP, LEVELS, ITERS, Q,
+                                                 radius=JBU_RADIUS)
             oracle.compact_cloud(hi, Q, 1.0)  # a8: the packed cloud, as the GPU path
 
     ts = [threading.Thread(target=work, args=(k,)) for k in range(n_threads)]
@@ -254,7 +280,7 @@ def run_reference(args):
         "data": "synthetic", "config": {"workload": WORKLOAD, "pairs_per_step": threads},
         "cpu_baseline": {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
                          "sample": f"{threads} pairs per step (one per host thread, consecutive frames of the "
-                                   f"C5 video), {args.steps} steps"},
+                                   f"C{CONFIG} video), {args.steps} steps"},
         "e2e": {"value": v, "unit": "pairs/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -284,6 +310,7 @@ def run_ours(args):
     I = q_intrinsics()
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(W_HI, H_HI, S_DOWN, NDISP, LEVELS, ITERS, batch=B, Q=Q, device=dev,
+                            radius=args.jbu_radius or None, msg_bytes=args.msg_bytes,
                             camera=CAMERA if args.rectify else None,
                             features=FEATURES if args.features else None, csbp_k0=args.csbp or None)
     full_bp = isinstance(pipe.bp, P.StereoBP)
@@ -422,7 +449,7 @@ def run_ours(args):
         fr = frames[0, : min(threads, B) + 1].cpu().numpy()
         v, n, dt = oracle_rate(threads, args.cpu_pairs, fr)
         cpu = {"value": v, "unit": "pairs/s", "cores": threads, "kind": "oracle",
-               "sample": f"{n} pairs of the same workload (consecutive frames of the C5 video), one thread per "
+               "sample": f"{n} pairs of the same workload (consecutive frames of the C{CONFIG} video), one thread per "
                          f"pair at a time ({dt:.1f} s)"}
 
     if rank == 0:
@@ -455,6 +482,13 @@ def run_ours(args):
 
 def main():
     args = parse()
+    set_config(args.config)
+    global JBU_RADIUS
+    JBU_RADIUS = args.jbu_radius or None
+    if not args.batch:
+        args.batch = 128 if args.config == 5 else 16
+    if args.config == 4 and args.cpu_pairs == 4:
+        args.cpu_pairs = 1  # the oracle takes ~22 s per C4 pair on one core
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)
