@@ -363,6 +363,7 @@ def run_ours(args):
         step(s)
     if full_bp:
         pipe.bp.timing_read()  # discard warm-up timings
+    P.jbu_timing(True)  # the JBU kernel's own CUDA events inside the timed steps (second roofline)
     barrier()
 
     sampler = ClockSampler(local_rank)
@@ -382,6 +383,8 @@ def run_ours(args):
     ms = e0.elapsed_time(e1)
     ms_max = max_over_ranks(ms)
     lv = pipe.bp.timing_read() if full_bp else None
+    jt = P.jbu_timing_read()
+    P.jbu_timing(False)
     pairs = world * B * args.steps
     value = pairs / (ms_max / 1000.0)
     n_valid_last = int(pipe.offsets[B].item()) if pipe.offsets is not None else None
@@ -442,6 +445,22 @@ def run_ours(args):
                     "lane-ops/clk/SM, tools/micro/alu_bench), so its HBM fraction is not its binding roofline",
         }
 
+    # ---- second roofline: the JBU kernel (a6 + the a8 counts), bound by MUFU.EX2 (one per
+    # pixel-tap); peak = 16 EX2 lanes / clk / SM (tools/micro/mufu_bench measured 15.8)
+    # x SMs x the SM clock sampled during the timed steps
+    roofline_jbu = None
+    if jt["launches"] > 0 and jt["ms"] > 0:
+        sms = torch.cuda.get_device_properties(dev).multi_processor_count
+        mhz = (clocks or {}).get("sm_mhz") or 1965.0
+        peak_t = 16.0 * sms * mhz * 1e6 / 1e9  # G pixel-taps/s
+        ach_t = (jt["taps"] / 1e9) / (jt["ms"] / 1e3)
+        roofline_jbu = {"kernel": "k_jbu_vec (a6 JBU + a8 segment counts)", "bound": "xu (MUFU.EX2)",
+                        "achieved": ach_t, "peak": peak_t, "unit": "G pixel-taps/s", "frac": ach_t / peak_t,
+                        "us_per_launch": 1000.0 * jt["ms"] / jt["launches"],
+                        "taps_per_launch": jt["taps"] / jt["launches"],
+                        "note": "one weight 2^x (one MUFU.EX2) per output pixel and window tap; peak from the "
+                                "nominal 16 EX2 lanes/clk/SM at the sampled SM clock"}
+
     # ---- CPU baseline: the oracle on this host's cores (rank 0 at N=1 only)
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
@@ -470,6 +489,7 @@ def run_ours(args):
                        "bp_msg_storage": f"u{8 * pipe.bp.params()['msg_bytes']}" if full_bp else "i32 (csbp)",
                        "jbu_arith": "f32"},
             "clocks": clocks, "gpu_launches": int(launches), "e2e": e2e, "roofline": roofline,
+            "roofline_jbu": roofline_jbu,
             "cpu_baseline": cpu,
             "per_level_update_ms_per_step": [x["ms"] / args.steps for x in lv] if lv else None,
             "last_batch_points": n_valid_last,

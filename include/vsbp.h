@@ -373,6 +373,16 @@ int pair_summary_batch(int B, const int32_t *disp_lo, int W, int H, const unsign
 int bp_timing_enable(vsbp_bp *ctx, int enable);
 int bp_timing_read(vsbp_bp *ctx, double *ms, int64_t *launches, double *bytes);
 
+/* Live timing of the JBU kernel (a6, with the a8 counts) inside jbu_compact_batch,
+ * for bench.py's second roofline: jbu_timing_enable(1) makes every later
+ * jbu_compact_batch record CUDA events around that kernel on its stream (process-wide;
+ * not thread-safe); jbu_timing_read synchronises them and returns, accumulated since
+ * the last read, the device ms, the launches and the algorithmic pixel-taps (B * sW *
+ * sH * (2r+1)^2: one weight, one 2^x, each).  Errors: VSBP_EINVAL (null pointers),
+ * VSBP_ECUDA. */
+int jbu_timing_enable(int enable);
+int jbu_timing_read(double *ms, long long *launches, double *taps);
+
 const char *vsbp_strerror(int code);
 
 /* Number of kernel launches this thread has enqueued through the library

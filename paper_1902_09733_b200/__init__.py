@@ -93,6 +93,8 @@ _EXPORTS = {
                                      C.c_void_p, C.c_void_p]),
     "bp_timing_enable": (C.c_int, [C.c_void_p, C.c_int]),
     "bp_timing_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "jbu_timing_enable": (C.c_int, [C.c_int]),
+    "jbu_timing_read": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "vsbp_q_matrix": (C.c_int, [C.c_double, C.c_double, C.c_double, C.c_double, C.c_double, C.c_void_p]),
     "compact_workspace_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
     "compact_cloud_batch": (C.c_int, [C.c_int, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_float, C.c_void_p,
@@ -495,6 +497,19 @@ class CloudCompactor:
                                          C.c_void_p(self.workspace.data_ptr()), self.workspace.numel(),
                                          _stream(stream)), "compact_cloud_batch")
         return xyz, offsets, n_valid
+
+
+def jbu_timing(enable: bool = True):
+    """Live CUDA-event timing of the JBU kernel inside every later jbu_compact call
+    (include/vsbp.h jbu_timing_enable)."""
+    _check(lib().jbu_timing_enable(1 if enable else 0), "jbu_timing_enable")
+
+
+def jbu_timing_read():
+    """{ms, launches, taps} accumulated since the last read (synchronises)."""
+    ms, n, taps = C.c_double(), C.c_longlong(), C.c_double()
+    _check(lib().jbu_timing_read(C.byref(ms), C.byref(n), C.byref(taps)), "jbu_timing_read")
+    return dict(ms=ms.value, launches=int(n.value), taps=taps.value)
 
 
 def jbu_compact(disp_lo: torch.Tensor, guide_rgb: torch.Tensor, s: int, sigma_s: float, sigma_r: float, radius: int,

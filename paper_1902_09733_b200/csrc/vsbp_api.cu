@@ -752,6 +752,64 @@ int compact_cloud_batch(int B, const float *disp, int W, int H, const double *Q,
     return VSBP_OK;
 }
 
+// ---- live timing of the JBU kernel inside jbu_compact_batch (bench.py's second roofline)
+namespace {
+struct JbuTiming {
+    int on = 0, head = 0, n = 0;
+    cudaEvent_t ev[64][2];
+    double taps[64];
+    double ms = 0.0, tap_sum = 0.0;
+    long long launches = 0;
+    bool created = false;
+} g_jt;
+
+int jt_drain(int block)
+{
+    while (g_jt.n > 0) {
+        const int i = g_jt.head;
+        if (!block) {
+            const cudaError_t q = cudaEventQuery(g_jt.ev[i][1]);
+            if (q == cudaErrorNotReady) break;
+            CK(q);
+        } else {
+            CK(cudaEventSynchronize(g_jt.ev[i][1]));
+        }
+        float ms = 0.f;
+        CK(cudaEventElapsedTime(&ms, g_jt.ev[i][0], g_jt.ev[i][1]));
+        g_jt.ms += ms;
+        g_jt.tap_sum += g_jt.taps[i];
+        ++g_jt.launches;
+        g_jt.head = (i + 1) % 64;
+        --g_jt.n;
+    }
+    return VSBP_OK;
+}
+}  // namespace
+
+int jbu_timing_enable(int enable)
+{
+    if (enable && !g_jt.created) {
+        for (int i = 0; i < 64; ++i)
+            for (int k = 0; k < 2; ++k) CK(cudaEventCreate(&g_jt.ev[i][k]));
+        g_jt.created = true;
+    }
+    g_jt.on = enable ? 1 : 0;
+    return VSBP_OK;
+}
+
+int jbu_timing_read(double *ms, long long *launches, double *taps)
+{
+    if (!ms || !launches || !taps) return VSBP_EINVAL;
+    const int rc = jt_drain(1);
+    if (rc) return rc;
+    *ms = g_jt.ms;
+    *launches = g_jt.launches;
+    *taps = g_jt.tap_sum;
+    g_jt.ms = g_jt.tap_sum = 0.0;
+    g_jt.launches = 0;
+    return VSBP_OK;
+}
+
 int jbu_compact_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t *guide_rgb, int s, float sigma_s,
                       float sigma_r, int radius, const double *Q, float min_disp, float *disp_hi, float *xyz,
                       long long cap_points, long long *offsets, unsigned long long *n_valid, void *workspace,
@@ -765,8 +823,22 @@ int jbu_compact_batch(int B, const int32_t *disp_lo, int W, int H, const uint8_t
     for (int i = 0; i < 16; ++i) Qf[i] = (float)Q[i];
     cudaStream_t st = (cudaStream_t)stream;
     CK(vsbp::compact_zero_counts(B, W * s, H * s, workspace, st));
+    int slot = -1;
+    if (g_jt.on) {
+        int rc2 = jt_drain(0);
+        if (!rc2 && g_jt.n == 64) rc2 = jt_drain(1);
+        if (rc2) return rc2;
+        slot = (g_jt.head + g_jt.n) % 64;
+        CK(cudaEventRecord(g_jt.ev[slot][0], st));
+    }
     CK(vsbp::launch_jbu_fast(B, disp_lo, W, H, guide_rgb, s, disp_hi, sigma_s, sigma_r, radius, nullptr, min_disp,
                              nullptr, nullptr, st, vsbp::compact_counts(workspace)));
+    if (slot >= 0) {
+        CK(cudaEventRecord(g_jt.ev[slot][1], st));
+        // the algorithmic work: one weight (one 2^x) per output pixel and window tap
+        g_jt.taps[slot] = (double)B * W * s * H * s * (2.0 * radius + 1) * (2.0 * radius + 1);
+        ++g_jt.n;
+    }
     CK(vsbp::launch_compact_from_counts(B, disp_hi, W * s, H * s, Qf, min_disp, xyz, cap_points, offsets, n_valid,
                                         workspace, st));
     return VSBP_OK;
