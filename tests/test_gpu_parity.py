@@ -919,3 +919,27 @@ def test_jbu_compact_equals_separate_calls(s, r, W, H, B):
     assert torch.equal(hi, hi2) and torch.equal(off, off2) and torch.equal(nv, nv2)
     assert torch.equal(xyz[: int(off[-1])], xyz2[: int(off2[-1])])
     assert int(off[-1]) == int((hi2 >= 1.0).sum())
+
+
+@pytest.mark.gpu
+def test_jbu_timing_counts_launches_and_taps():
+    """jbu_timing_enable / read (bench.py's second roofline): one record per
+    jbu_compact call, taps = B * sW * sH * (2r+1)^2, positive device time; nothing is
+    recorded once disabled."""
+    s, r, W, H, B = 4, 2, 64, 40, 2
+    rng = np.random.default_rng(3)
+    lo = to_dev(rng.integers(0, 20, size=(B, H, W)).astype(np.int32))
+    guide = to_dev(np.stack([synthgen.value_noise_rgb(b + 1, W * s, H * s) for b in range(B)]))
+    Q = P.q_matrix(900.0, 880.0, W * s / 2, H * s / 2, 0.5)
+    comp = P.CloudCompactor(W * s, H * s, B, device=dev())
+    P.jbu_timing_read()  # drop anything earlier
+    P.jbu_timing(True)
+    for _ in range(3):
+        P.jbu_compact(lo, guide, s, 3.75, 15.0, r, Q, 1.0, comp)
+    t = P.jbu_timing_read()
+    P.jbu_timing(False)
+    P.jbu_compact(lo, guide, s, 3.75, 15.0, r, Q, 1.0, comp)
+    t2 = P.jbu_timing_read()
+    assert t["launches"] == 3 and t["ms"] > 0
+    assert t["taps"] == 3 * B * W * s * H * s * (2 * r + 1) ** 2
+    assert t2["launches"] == 0 and t2["taps"] == 0
