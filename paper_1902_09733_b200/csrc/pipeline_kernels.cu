@@ -189,8 +189,25 @@ __global__ void __launch_bounds__(256) k_summary(const int32_t *__restrict__ dis
     const int b = blockIdx.y;
     long long sum = 0;
     unsigned long long hash = 0;
-    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < N; i += gridDim.x * blockDim.x) {
-        const int d = disp[(size_t)b * N + i];
+    const int32_t *src = disp + (size_t)b * N;
+    const int t0 = blockIdx.x * blockDim.x + threadIdx.x, stride = gridDim.x * blockDim.x;
+    int i0 = 0;
+    if ((N & 3) == 0 && ((uintptr_t)src & 15) == 0) {
+        // four labels per 16-byte load (order-independent sums: same result)
+        const int4 *s4 = reinterpret_cast<const int4 *>(src);
+        for (int q = t0; q < N / 4; q += stride) {
+            const int4 v = __ldg(s4 + q);
+            const int d[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+                sum += d[k];
+                hash += mix64(((unsigned long long)(4 * q + k) << 32) | (unsigned)d[k]);
+            }
+        }
+        i0 = N;
+    }
+    for (int i = i0 + t0; i < N; i += stride) {
+        const int d = src[i];
         sum += d;
         hash += mix64(((unsigned long long)i << 32) | (unsigned)d);
     }
