@@ -170,7 +170,13 @@ bool use_pair(const vsbp_bp *c, int l, int B)
     // each pair >= 10K (C5 level 1 fused 8466 -> 8586 pairs/s, level 2 with
     // 16-row bands 8611 -> 8638; C4 level 1 0.191 -> 0.183 ms per pair; C4 level 2
     // (64K px x 8 pairs) 0.052 -> 0.066 ms)
-    return px >= 10000 && px * B >= 2000000;
+#ifndef VSBP_U16_MIN_PX
+#define VSBP_U16_MIN_PX 10000
+#endif
+#ifndef VSBP_U16_MIN_BATCH_PX
+#define VSBP_U16_MIN_BATCH_PX 2000000
+#endif
+    return px >= VSBP_U16_MIN_PX && px * B >= VSBP_U16_MIN_BATCH_PX;
 }
 
 // rows per CTA band of k_update_pair on level l: pair_band, and 16 on levels shorter
