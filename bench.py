@@ -77,9 +77,9 @@ def parse():
                    help="BASELINE.json config: 5 = the C5 stream (default, the headline); 4 = the C4 resolution "
                         "(1352x760, L = 128, 6 x 8) on the same stream")
     p.add_argument("--batch", type=int, default=0,
-                   help="pairs per GPU per step (default 128 at C5 -- measured 32 / 64 / 96 / 128 / 160 -> "
-                        "6865 / 7041 / 7102 / 7135 / 7127 pairs/s in round 1 -- and 16 at C4, whose BP state is "
-                        "1.4 GB per pair)")
+                   help="pairs per GPU per step (default 256 at C5 -- measured 96 / 128 / 192 / 256 -> "
+                        "8550 / 8662 / 8759 / 8805 pairs/s; 51.6 GB of BP state -- and 16 at C4, whose BP state "
+                        "is 1.4 GB per pair)")
     p.add_argument("--jbu-radius", type=int, default=0, help="JBU window radius (default ceil(5 / s): 2 at C5)")
     p.add_argument("--msg-bytes", type=int, default=0, choices=[0, 1, 2, 4],
                    help="BP message storage bytes (0: the smallest lossless, u8 here)")
@@ -506,7 +506,7 @@ def main():
     global JBU_RADIUS
     JBU_RADIUS = args.jbu_radius or None
     if not args.batch:
-        args.batch = 128 if args.config == 5 else 16
+        args.batch = 256 if args.config == 5 else 16
     if args.config == 4 and args.cpu_pairs == 4:
         args.cpu_pairs = 1  # the oracle takes ~22 s per C4 pair on one core
     if args.impl == "reference":

@@ -692,14 +692,14 @@ def test_icp_failure_and_identity():
 
 # ----------------------------------------------------------------------------- bench configuration
 def test_bench_launch_configuration_sampled_pairs():
-    """The configuration bench.py times (C5: one batch of 128 pairs = 129 consecutive
+    """The configuration bench.py times (C5: one batch of 256 pairs = 257 consecutive
     frames of the synthetic 2.7K video, s=4, L=64, 5x5, JBU r=2, packed clouds):
     three sampled pairs of a batch deep into the stream (first, middle, last) through
     the whole path against the oracle -- disparities bit-exact, JBU within 1e-4 px,
     the packed cloud's counts exact and its points within 1e-5 relative."""
     import bench
     from synthgen import video
-    B = 128
+    B = 256
     I = synthgen.INTRINSICS
     Q = P.q_matrix(I["f_du"], I["f_dv"], I["u0"], I["v0"], I["B"])
     pipe = P.StereoPipeline(bench.W_HI, bench.H_HI, bench.S_DOWN, bench.NDISP, bench.LEVELS, bench.ITERS, batch=B,

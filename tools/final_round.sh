@@ -14,7 +14,7 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench_$TAG.json 2> gpurun_out/bench_$TAG.err; echo "bench rc=$?"
 timeout 900 python bench.py --impl reference --steps 2 --warmup 1 > gpurun_out/bench_ref_$TAG.json 2> gpurun_out/bench_ref_$TAG.err; echo "ref rc=$?"
 [ -n "$SKIP_ROWS" ] || { timeout 900 python tools/bench_rows.py --out gpurun_out/rows_$TAG.json > /dev/null 2> gpurun_out/rows_$TAG.err; echo "rows rc=$?"; }
-ARGS="--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 256"
+ARGS="--batch 256 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 512"
 timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -c 400 --csv \
     --log-file gpurun_out/launches_$TAG.csv python bench.py $ARGS > gpurun_out/ncu_launch_$TAG.log 2>&1; echo "launch list rc=$?"
 # k_update_pair launches per step: levels 2 and 1 (u16: MODE 2, MODE 0 each), then level 0 (MODE 2,

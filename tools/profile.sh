@@ -7,7 +7,7 @@
 TAG=${1:-run}
 shift
 CAPS=${@:-"k_update_fast:21 k_jbu_fast:1"}
-ARGS=${PROFILE_ARGS:-"--batch 128 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 256"}
+ARGS=${PROFILE_ARGS:-"--batch 256 --steps 2 --warmup 1 --no-e2e --no-cpu-baseline --pairs 512"}
 mkdir -p gpurun_out
 timeout 600 python bench.py $ARGS > gpurun_out/plain_$TAG.log 2>&1 || { echo "plain run failed"; exit 1; }
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv \
